@@ -1,0 +1,1031 @@
+// Device plans and the C-ABI products (include/csrc_gpu.h).
+//
+// A plan is the GPU counterpart of csrc::ParallelSpmv (parallel.hpp:151-446):
+// it owns a device copy of the CSRC arrays, the schedule (bands/tiles, ring
+// windows, colour classes, private buffers) and a stream; apply() enqueues
+// init / compute / accumulate phases and records PhaseTimings-style events.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "internal.hpp"
+#include "kernels.cuh"
+
+using namespace csrcgpu;
+
+namespace {
+
+#define CUDA_OK(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            throw Error(std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " + \
+                        #expr);                                                         \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    void alloc(size_t b) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = b;
+        // 256 B of slack past the end keeps vector tail loads in bounds
+        CUDA_OK(cudaMalloc(&p, std::max<size_t>(b, 1) + 256));
+    }
+    template <class U>
+    U* as() const { return static_cast<U*>(p); }
+};
+
+template <class U>
+void upload(DevBuf& d, const U* h, size_t count) {
+    d.alloc(count * sizeof(U));
+    if (count) CUDA_OK(cudaMemcpy(d.p, h, count * sizeof(U), cudaMemcpyHostToDevice));
+}
+
+int num_sms(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    return v > 0 ? v : 148;
+}
+
+int pow2_at_least(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return static_cast<int>(p);
+}
+
+}  // namespace
+
+struct csrc_gpu_plan_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int kind = CSRC_KIND_WINDOWED;
+    int accum = CSRC_ACCUM_EFFECTIVE;
+    int dtype = CSRC_DTYPE_F64;
+    int p_ref = 1;
+    int exec_kind = CSRC_KIND_WINDOWED;  // what actually runs
+    bool value_symmetric = false;
+    index_t n_global = 0;
+    index_t row_begin = 0, row_end = 0, lo = 0;
+    index_t nrows = 0;
+    count_t k = 0;
+    count_t nnz_stored = 0;
+    int sub_lanes = 16;  // atomic / colored lanes per row
+
+    DevBuf ia, ja, al, au, ad;  // matrix (dtype values)
+
+    // windowed / local buffers
+    int bands = 0;
+    DevBuf tile_start, band_tile, band_shift;
+    int near_depth = 0, far_lo = 1, far_hi = 0, ring_near = 1, ring_far = 1;
+    int max_tile_pairs = 8192;
+    size_t win_smem = 0;
+    double captured = 0.0;
+    // band plans: boundary / interior sub-schedules
+    index_t split = 0;
+    int bands_part[2] = {0, 0};
+    DevBuf tile_part[2], band_tile_part[2];
+
+    // local buffers
+    DevBuf buf, boff, blo, bhi, bstart, iv_begin, iv_end, cptr, contrib;
+    int n_iv = 0;
+    count_t buf_total = 0;
+
+    // colorful (class-major copy)
+    int n_colors = 0;
+    std::vector<count_t> class_ptr;
+    DevBuf rid, cia, cja, cal, cau, cad;
+
+    // host-path scratch
+    DevBuf dx, dy, dxd, dyd, flushbuf;
+
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool ev_recorded = false;
+
+    // graph cache
+    cudaGraphExec_t graph = nullptr;
+    const void* g_x = nullptr;
+    void* g_y = nullptr;
+    cudaStream_t g_stream = nullptr;
+
+    size_t vsize() const { return dtype == CSRC_DTYPE_F32 ? 4 : 8; }
+    index_t vec_len() const { return row_end - lo; }
+    int launches = 0;
+
+    ~csrc_gpu_plan_s() {
+        if (graph) cudaGraphExecDestroy(graph);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+using Plan = csrc_gpu_plan_s;
+
+// ---------------------------------------------------------- uploads
+template <class T>
+void upload_values(DevBuf& d, const double* h, size_t count) {
+    if (std::is_same<T, double>::value) {
+        upload(d, h, count);
+    } else {
+        std::vector<float> tmp(count);
+        for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(h[i]);
+        upload(d, tmp.data(), count);
+    }
+}
+
+// --------------------------------------------------- windowed schedule
+// Ring windows from the histogram of scatter distances d = row - ja:
+// near covers 1..Dn (plus the own row), far the densest window beyond Dn.
+void choose_windows(Plan& P, const MatView& a) {
+    const int T = dev::kTileRows;
+    const int kRingMax = 2048;
+    count_t maxd = 0;
+    for (index_t r = P.row_begin; r < P.row_end; ++r)
+        if (a.ia[r + 1] > a.ia[r]) maxd = std::max<count_t>(maxd, r - a.ja[a.ia[r]]);
+    std::vector<count_t> hist(static_cast<size_t>(maxd) + 2, 0);
+    for (index_t r = P.row_begin; r < P.row_end; ++r)
+        for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) ++hist[r - a.ja[t]];
+    const count_t total = a.ia[P.row_end] - a.ia[P.row_begin];
+    int dn_cap = kRingMax - T;
+    int dn = 0;
+    count_t near_cnt = 0;
+    for (count_t d = 1; d <= std::min<count_t>(maxd, dn_cap); ++d)
+        if (hist[d]) {
+            dn = static_cast<int>(d);
+            near_cnt += hist[d];
+        }
+    P.near_depth = dn;
+    P.ring_near = pow2_at_least(dn + T);
+    P.far_lo = 1;
+    P.far_hi = 0;
+    P.ring_far = 1;
+    count_t far_cnt = 0;
+    if (maxd > dn) {
+        const int W = kRingMax - T;  // window width in distances
+        count_t best = 0, cur = 0;
+        count_t best_lo = dn + 1;
+        count_t lo = dn + 1;
+        for (count_t hi = dn + 1; hi <= maxd; ++hi) {
+            cur += hist[hi];
+            while (hi - lo > W) cur -= hist[lo++];
+            if (cur > best) {
+                best = cur;
+                best_lo = lo;
+            }
+        }
+        if (best > 0 && best * 50 >= total) {  // worth a ring if >= 2% of pairs
+            count_t f0 = best_lo, f1 = std::min<count_t>(best_lo + W, maxd);
+            while (f0 < f1 && hist[f0] == 0) ++f0;
+            while (f1 > f0 && hist[f1] == 0) --f1;
+            P.far_lo = static_cast<int>(f0);
+            P.far_hi = static_cast<int>(f1);
+            P.ring_far = pow2_at_least(f1 - f0 + 1 + T);
+            far_cnt = best;
+        }
+    }
+    P.captured = total ? static_cast<double>(near_cnt + far_cnt) / total : 1.0;
+}
+
+// Tiles (<= kTileRows rows, <= max_tile_pairs pairs) over bands given as
+// local row starts bs[0..nb].
+void build_tiles(Plan& P, const MatView& a, const std::vector<index_t>& bs, DevBuf& d_tiles,
+                 DevBuf& d_band_tile) {
+    std::vector<int32_t> tiles, band_tile;
+    const int nb = static_cast<int>(bs.size()) - 1;
+    for (int b = 0; b < nb; ++b) {
+        band_tile.push_back(static_cast<int32_t>(tiles.size()));
+        index_t r = bs[b];
+        const index_t e = bs[b + 1];
+        while (r < e) {
+            tiles.push_back(r);
+            index_t end = std::min<index_t>(r + dev::kTileRows, e);
+            const index_t g = P.row_begin;
+            while (end > r + 1 &&
+                   static_cast<count_t>(a.ia[g + end]) - a.ia[g + r] > P.max_tile_pairs) {
+                end = r + 1 + (end - r - 1) / 2;
+            }
+            // grow back greedily after the halving overshoot
+            while (end < std::min<index_t>(r + dev::kTileRows, e) &&
+                   static_cast<count_t>(a.ia[g + end + 1]) - a.ia[g + r] <= P.max_tile_pairs)
+                ++end;
+            r = end;
+        }
+    }
+    band_tile.push_back(static_cast<int32_t>(tiles.size()));
+    tiles.push_back(bs[nb]);
+    upload(d_tiles, tiles.data(), tiles.size());
+    upload(d_band_tile, band_tile.data(), band_tile.size());
+}
+
+template <class T>
+size_t windowed_smem(const Plan& P) {
+    const bool far_on = P.far_lo <= P.far_hi;
+    size_t s = sizeof(T) * (P.ring_near + (far_on ? P.ring_far : 0) + dev::kTileRows);
+    s += sizeof(int32_t) * (dev::kTileRows + 1);
+    s += sizeof(uint16_t) * P.max_tile_pairs;
+    return (s + 15) & ~size_t(15);
+}
+
+template <class T>
+int windowed_blocks_per_sm(const Plan& P) {
+    cudaFuncSetAttribute(dev::k_windowed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(P.win_smem));
+    int nb = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::k_windowed<T>,
+                                                         dev::kWarpsPerCta * 32, P.win_smem));
+    if (nb < 1) throw Error("windowed kernel does not fit on an SM (smem " +
+                            std::to_string(P.win_smem) + " B)");
+    return nb;
+}
+
+// local sub-view of rows [row_begin, row_end) for partition_by_nnz
+MatView local_view(const MatView& a, index_t r0, index_t r1) {
+    MatView v = a;
+    v.n = r1 - r0;
+    v.ia = a.ia + r0;
+    v.k = a.ia[r1] - a.ia[r0];
+    return v;
+}
+
+template <class T>
+void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
+                    int requested_bands) {
+    choose_windows(P, a);
+    count_t max_row = 0;
+    for (index_t r = P.row_begin; r < P.row_end; ++r)
+        max_row = std::max<count_t>(max_row, a.ia[r + 1] - a.ia[r]);
+    P.max_tile_pairs = static_cast<int>(std::max<count_t>(8192, max_row));
+    if (P.max_tile_pairs > 65536) P.max_tile_pairs = static_cast<int>(max_row);
+    P.win_smem = windowed_smem<T>(P);
+    if (P.win_smem > 227 * 1024)
+        throw Error("windowed: row with " + std::to_string(max_row) +
+                    " pairs exceeds the shared-memory tile budget");
+    const int per_sm = windowed_blocks_per_sm<T>(P);
+    std::vector<index_t> bs;
+    if (explicit_bs) {
+        bs = *explicit_bs;
+    } else {
+        int bands = requested_bands > 0 ? requested_bands : num_sms(P.device) * per_sm;
+        bands = static_cast<int>(std::min<count_t>(bands, std::max<count_t>(1, P.nrows / 64)));
+        bands = std::max(1, std::min<int>(bands, P.nrows));
+        RowPartition part = partition_by_nnz(local_view(a, P.row_begin, P.row_end), bands);
+        bs = part.block_start;
+    }
+    P.bands = static_cast<int>(bs.size()) - 1;
+    build_tiles(P, a, bs, P.tile_start, P.band_tile);
+    if (P.row_begin > 0 || P.row_end < P.n_global) {
+        // band plan: boundary rows [row_begin, split) scatter below row_begin
+        index_t split = P.row_begin;
+        for (index_t r = P.row_begin; r < P.row_end; ++r)
+            if (a.ia[r + 1] > a.ia[r] && a.ja[a.ia[r]] < P.row_begin) split = r + 1;
+        P.split = split;
+        const index_t parts[3] = {0, split - P.row_begin, P.nrows};
+        for (int q = 0; q < 2; ++q) {
+            const index_t rows = parts[q + 1] - parts[q];
+            if (rows <= 0) {
+                P.bands_part[q] = 0;
+                std::vector<index_t> none = {parts[q]};
+                build_tiles(P, a, none, P.tile_part[q], P.band_tile_part[q]);
+                continue;
+            }
+            int nb = std::max(1, std::min<int>(num_sms(P.device) * per_sm,
+                                               static_cast<int>(rows / 64)));
+            RowPartition part = partition_by_nnz(
+                local_view(a, P.row_begin + parts[q], P.row_begin + parts[q + 1]), nb);
+            for (auto& v : part.block_start) v += parts[q];
+            P.bands_part[q] = nb;
+            build_tiles(P, a, part.block_start, P.tile_part[q], P.band_tile_part[q]);
+        }
+    }
+}
+
+template <class T>
+dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose) {
+    dev::WinArgs<T> A{};
+    A.ia = P.ia.as<int32_t>();
+    A.ja = P.ja.as<int32_t>();
+    A.al = transpose ? P.au.as<T>() : P.al.as<T>();
+    A.au = transpose ? P.al.as<T>() : P.au.as<T>();
+    A.ad = P.ad.as<T>();
+    A.x = static_cast<const T*>(x);
+    A.out = static_cast<T*>(out);
+    A.tile_start = P.tile_start.as<int32_t>();
+    A.band_tile = P.band_tile.as<int32_t>();
+    A.band_shift = nullptr;
+    A.shift = -static_cast<int64_t>(P.lo);
+    A.xshift = -static_cast<int64_t>(P.lo);
+    A.row_begin = P.row_begin;
+    A.near_depth = P.near_depth;
+    A.far_lo = P.far_lo;
+    A.far_hi = P.far_hi;
+    A.ring_near = P.ring_near;
+    A.ring_far = P.ring_far;
+    A.max_tile_pairs = P.max_tile_pairs;
+    return A;
+}
+
+// ------------------------------------------------------- local buffers
+template <class T>
+void setup_buffers(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
+                   int requested_bands) {
+    setup_windowed<T>(P, a, explicit_bs, requested_bands);
+    // band starts (global) from the tiles: recompute from the schedule input
+    std::vector<int32_t> tiles(P.tile_start.bytes / 4), band_tile(P.band_tile.bytes / 4);
+    CUDA_OK(cudaMemcpy(tiles.data(), P.tile_start.p, P.tile_start.bytes, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(band_tile.data(), P.band_tile.p, P.band_tile.bytes,
+                       cudaMemcpyDeviceToHost));
+    std::vector<index_t> bs(P.bands + 1);
+    for (int b = 0; b <= P.bands; ++b) bs[b] = tiles[band_tile[b]];
+    std::vector<index_t> lo, hi;
+    effective_ranges(a, bs, lo, hi);
+    std::vector<int64_t> off(P.bands + 1, 0), shift(P.bands);
+    for (int b = 0; b < P.bands; ++b) {
+        off[b + 1] = off[b] + (hi[b] - lo[b] + 1);
+        shift[b] = off[b] - lo[b];
+    }
+    P.buf_total = off[P.bands];
+    IntervalPlan ip = build_interval_plan(lo, hi);
+    P.n_iv = static_cast<int>(ip.iv_begin.size());
+    P.buf.alloc(static_cast<size_t>(P.buf_total) * sizeof(T));
+    upload(P.boff, off.data(), off.size());
+    upload(P.band_shift, shift.data(), shift.size());
+    upload(P.blo, lo.data(), lo.size());
+    upload(P.bhi, hi.data(), hi.size());
+    upload(P.bstart, bs.data(), bs.size());
+    upload(P.iv_begin, ip.iv_begin.data(), ip.iv_begin.size());
+    upload(P.iv_end, ip.iv_end.data(), ip.iv_end.size());
+    upload(P.cptr, ip.contrib_ptr.data(), ip.contrib_ptr.size());
+    upload(P.contrib, ip.contrib.data(), ip.contrib.size());
+}
+
+template <class T>
+dev::BufArgs<T> buf_args(const Plan& P) {
+    dev::BufArgs<T> B{};
+    B.buf = P.buf.as<T>();
+    B.boff = P.boff.as<int64_t>();
+    B.blo = P.blo.as<int32_t>();
+    B.bhi = P.bhi.as<int32_t>();
+    B.bstart = P.bstart.as<int32_t>();
+    B.iv_begin = P.iv_begin.as<int32_t>();
+    B.iv_end = P.iv_end.as<int32_t>();
+    B.cptr = P.cptr.as<int32_t>();
+    B.contrib = P.contrib.as<int32_t>();
+    B.n_iv = P.n_iv;
+    B.p = P.bands;
+    B.total = P.buf_total;
+    return B;
+}
+
+// ------------------------------------------------------------- colorful
+template <class T>
+void setup_colored(Plan& P, const MatView& a, const std::vector<int32_t>& color, int n_colors) {
+    P.n_colors = n_colors;
+    const index_t n = a.n;
+    P.class_ptr.assign(n_colors + 1, 0);
+    for (index_t i = 0; i < n; ++i) ++P.class_ptr[color[i] + 1];
+    for (int c = 0; c < n_colors; ++c) P.class_ptr[c + 1] += P.class_ptr[c];
+    std::vector<int32_t> rows(n);
+    {
+        std::vector<count_t> next(P.class_ptr.begin(), P.class_ptr.end() - 1);
+        for (index_t i = 0; i < n; ++i) rows[next[color[i]]++] = i;  // ascending per class
+    }
+    std::vector<int64_t> cia(static_cast<size_t>(n) + 1, 0);
+    for (index_t r = 0; r < n; ++r) cia[r + 1] = cia[r] + (a.ia[rows[r] + 1] - a.ia[rows[r]]);
+    std::vector<int32_t> cja(static_cast<size_t>(a.k));
+    std::vector<double> cal(static_cast<size_t>(a.k)), cau, cad(n);
+    if (!a.value_symmetric) cau.resize(static_cast<size_t>(a.k));
+    for (index_t r = 0; r < n; ++r) {
+        const index_t i = rows[r];
+        cad[r] = a.ad[i];
+        count_t q = cia[r];
+        for (index_t t = a.ia[i]; t < a.ia[i + 1]; ++t, ++q) {
+            cja[q] = a.ja[t];
+            cal[q] = a.al[t];
+            if (!a.value_symmetric) cau[q] = a.au[t];
+        }
+    }
+    upload(P.rid, rows.data(), rows.size());
+    upload(P.cia, cia.data(), cia.size());
+    upload(P.cja, cja.data(), cja.size());
+    upload_values<T>(P.cal, cal.data(), cal.size());
+    if (!a.value_symmetric) upload_values<T>(P.cau, cau.data(), cau.size());
+    upload_values<T>(P.cad, cad.data(), cad.size());
+}
+
+int pick_lanes(count_t k, index_t n) {
+    const double avg = n ? static_cast<double>(k) / n : 1.0;
+    if (avg <= 2.5) return 2;
+    if (avg <= 5) return 4;
+    if (avg <= 10) return 8;
+    if (avg <= 20) return 16;
+    return 32;
+}
+
+// -------------------------------------------------------------- creation
+struct CreateOpts {
+    const int32_t* color = nullptr;
+    int32_t n_colors = 0;
+    const int32_t* block_start = nullptr;
+    int32_t bands = 0;
+    bool band = false;
+    index_t row_begin = 0, row_end = 0;
+};
+
+template <class T>
+void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const CreateOpts& o) {
+    const index_t r0 = P.row_begin, r1 = P.row_end;
+    const count_t t0 = a.ia[r0], t1 = a.ia[r1];
+    P.k = t1 - t0;
+    P.nrows = r1 - r0;
+    P.value_symmetric = a.value_symmetric;
+    P.nnz_stored = a.nnz_stored();
+    P.sub_lanes = pick_lanes(P.k, P.nrows);
+    // device arrays (band rows only)
+    {
+        std::vector<int32_t> ia_loc(static_cast<size_t>(P.nrows) + 1);
+        for (index_t r = 0; r <= P.nrows; ++r) ia_loc[r] = a.ia[r0 + r] - static_cast<int32_t>(t0);
+        upload(P.ia, ia_loc.data(), ia_loc.size());
+    }
+    const bool colored = P.exec_kind == CSRC_KIND_COLORFUL;
+    if (!colored) {
+        upload(P.ja, a.ja + t0, static_cast<size_t>(P.k));
+        upload_values<T>(P.al, a.al + t0, static_cast<size_t>(P.k));
+        if (!a.value_symmetric) upload_values<T>(P.au, a.au + t0, static_cast<size_t>(P.k));
+        upload_values<T>(P.ad, a.ad + r0, static_cast<size_t>(P.nrows));
+    }
+    switch (P.exec_kind) {
+        case CSRC_KIND_WINDOWED: {
+            std::vector<index_t> bs;
+            if (o.block_start) bs.assign(o.block_start, o.block_start + o.bands + 1);
+            setup_windowed<T>(P, a, o.block_start ? &bs : nullptr, s.bands);
+            P.launches = 2;
+            break;
+        }
+        case CSRC_KIND_LOCAL_BUFFERS: {
+            std::vector<index_t> bs;
+            if (o.block_start) bs.assign(o.block_start, o.block_start + o.bands + 1);
+            setup_buffers<T>(P, a, o.block_start ? &bs : nullptr, s.bands);
+            P.launches = 3;
+            break;
+        }
+        case CSRC_KIND_COLORFUL: {
+            std::vector<int32_t> color;
+            int nc = 0;
+            if (o.color) {
+                color.assign(o.color, o.color + a.n);
+                nc = o.n_colors;
+            } else {
+                color = color_rows(a, s.conflict_mode, s.color_order, &nc);
+            }
+            Validity v = validate_coloring(a, color.data(), nc);
+            if (!v.valid)
+                throw Error("coloring violation: rows " + std::to_string(v.row_a) + " and " +
+                            std::to_string(v.row_b) + " both write y[" +
+                            std::to_string(v.position) + "]");
+            setup_colored<T>(P, a, color, nc);
+            P.launches = 1 + nc;
+            break;
+        }
+        case CSRC_KIND_ATOMIC:
+            P.launches = 2;
+            break;
+        default:
+            throw Error("unknown strategy kind " + std::to_string(P.exec_kind));
+    }
+}
+
+Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const CreateOpts& o) {
+    if (!s) throw Error("null strategy");
+    MatView a = view_of(m, true);
+    // ParallelSpmv ctor checks (parallel.hpp:229-234)
+    if (s->p < 1) throw Error("ParallelSpmv: thread count must be >= 1");
+    if (s->kind == CSRC_KIND_SEQUENTIAL && s->p != 1)
+        throw Error("ParallelSpmv: sequential strategy requires p = 1");
+    if (s->kind < CSRC_KIND_SEQUENTIAL || s->kind > CSRC_KIND_WINDOWED)
+        throw Error("unknown strategy kind " + std::to_string(s->kind));
+    if (s->dtype != CSRC_DTYPE_F64 && s->dtype != CSRC_DTYPE_F32)
+        throw Error("unknown dtype " + std::to_string(s->dtype));
+    if (s->kind == CSRC_KIND_LOCAL_BUFFERS &&
+        (s->accum < CSRC_ACCUM_ALL_IN_ONE || s->accum > CSRC_ACCUM_INTERVAL))
+        throw Error("unknown accumulation method " + std::to_string(s->accum));
+    if (o.color && s->kind != CSRC_KIND_COLORFUL)
+        throw Error("ParallelSpmv: colorful plan given to a different strategy");
+    if (o.block_start) {
+        if (s->kind != CSRC_KIND_LOCAL_BUFFERS && s->kind != CSRC_KIND_WINDOWED)
+            throw Error("ParallelSpmv: local-buffers plan given to a different strategy");
+        if (s->kind == CSRC_KIND_LOCAL_BUFFERS && s->p >= 2 && o.bands != s->p)
+            throw Error("ParallelSpmv: plan built for p=" + std::to_string(o.bands) +
+                        ", strategy has p=" + std::to_string(s->p));
+        if (o.bands < 1 || o.block_start[0] != 0 || o.block_start[o.bands] != a.n)
+            throw Error("partition must cover rows [0, n)");
+        for (int b = 0; b < o.bands; ++b)
+            if (o.block_start[b + 1] <= o.block_start[b])
+                throw Error("effective_range: empty block");
+    }
+    if (o.color) {
+        if (o.n_colors < 1 && a.n > 0) throw Error("coloring has no classes");
+        for (index_t i = 0; i < a.n; ++i)
+            if (o.color[i] < 0 || o.color[i] >= o.n_colors)
+                throw Error("coloring: row " + std::to_string(i) + " colour out of range");
+    }
+    auto P = std::make_unique<Plan>();
+    P->device = s->device;
+    CUDA_OK(cudaSetDevice(P->device));
+    P->kind = s->kind;
+    P->accum = s->accum;
+    P->dtype = s->dtype;
+    P->p_ref = s->p;
+    P->n_global = a.n;
+    if (o.band) {
+        if (o.row_begin < 0 || o.row_end > a.n || o.row_begin >= o.row_end)
+            throw Error("band rows must satisfy 0 <= row_begin < row_end <= n");
+        P->row_begin = o.row_begin;
+        P->row_end = o.row_end;
+        index_t lo = o.row_begin;
+        for (index_t t = a.ia[o.row_begin]; t < a.ia[o.row_end]; ++t) lo = std::min(lo, a.ja[t]);
+        P->lo = lo;
+    } else {
+        P->row_begin = 0;
+        P->row_end = a.n;
+        P->lo = 0;
+    }
+    // what runs: p = 1 or sequential short-circuit (parallel.hpp:197-202) -> windowed, no buffers
+    P->exec_kind = s->kind;
+    if (s->kind == CSRC_KIND_SEQUENTIAL) P->exec_kind = CSRC_KIND_WINDOWED;
+    if (s->kind == CSRC_KIND_LOCAL_BUFFERS && s->p < 2 && !o.block_start)
+        P->exec_kind = CSRC_KIND_WINDOWED;
+    if (o.band && (P->exec_kind == CSRC_KIND_LOCAL_BUFFERS || P->exec_kind == CSRC_KIND_COLORFUL))
+        throw Error("band plans support the windowed and atomic kernels only");
+    CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev) CUDA_OK(cudaEventCreate(&e));
+    if (a.n == 0) return P.release();
+    if (P->dtype == CSRC_DTYPE_F64)
+        create_typed<double>(*P, a, *s, o);
+    else
+        create_typed<float>(*P, a, *s, o);
+    return P.release();
+}
+
+// --------------------------------------------------------------- apply
+int grid_for(int device, int64_t work, int per_block) {
+    int64_t blocks = (work + per_block - 1) / per_block;
+    const int64_t cap = static_cast<int64_t>(num_sms(device)) * 16;
+    return static_cast<int>(std::max<int64_t>(1, std::min(blocks, cap)));
+}
+
+template <class T, int L>
+void launch_atomic_L(const Plan& P, const T* al, const T* au, const T* x, T* y, cudaStream_t st) {
+    const int rows_per_block = 256 / L;
+    dev::k_atomic<T, L><<<grid_for(P.device, P.nrows, rows_per_block), 256, 0, st>>>(
+        P.ia.as<int32_t>(), P.ja.as<int32_t>(), al, au, P.ad.as<T>(), x, y, P.nrows,
+        P.row_begin, -static_cast<int64_t>(P.lo));
+}
+
+template <class T, int L>
+void launch_colored_L(const Plan& P, const T* al, const T* au, const T* x, T* y,
+                      cudaStream_t st) {
+    for (int c = 0; c < P.n_colors; ++c) {
+        const count_t c0 = P.class_ptr[c], c1 = P.class_ptr[c + 1];
+        if (c1 <= c0) continue;
+        dev::k_colored<T, L><<<grid_for(P.device, c1 - c0, 256 / L), 256, 0, st>>>(
+            P.rid.as<int32_t>(), P.cia.as<int64_t>(), P.cja.as<int32_t>(), al, au,
+            P.cad.as<T>(), x, y, c0, c1, -static_cast<int64_t>(P.lo));
+    }
+}
+
+template <class T>
+void launch_atomic(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    const T* al = (tr ? P.au : P.al).template as<T>();
+    const T* au = (tr ? P.al : P.au).template as<T>();
+    if (P.value_symmetric) au = al = P.al.as<T>();
+    switch (P.sub_lanes) {
+        case 2: launch_atomic_L<T, 2>(P, al, au, x, y, st); break;
+        case 4: launch_atomic_L<T, 4>(P, al, au, x, y, st); break;
+        case 8: launch_atomic_L<T, 8>(P, al, au, x, y, st); break;
+        case 16: launch_atomic_L<T, 16>(P, al, au, x, y, st); break;
+        default: launch_atomic_L<T, 32>(P, al, au, x, y, st); break;
+    }
+}
+
+template <class T>
+void launch_colored(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    const T* al = (tr ? P.cau : P.cal).template as<T>();
+    const T* au = (tr ? P.cal : P.cau).template as<T>();
+    if (P.value_symmetric) au = al = P.cal.as<T>();
+    switch (P.sub_lanes) {
+        case 2: launch_colored_L<T, 2>(P, al, au, x, y, st); break;
+        case 4: launch_colored_L<T, 4>(P, al, au, x, y, st); break;
+        case 8: launch_colored_L<T, 8>(P, al, au, x, y, st); break;
+        case 16: launch_colored_L<T, 16>(P, al, au, x, y, st); break;
+        default: launch_colored_L<T, 32>(P, al, au, x, y, st); break;
+    }
+}
+
+template <class T>
+void launch_windowed(const Plan& P, dev::WinArgs<T> A, int bands, cudaStream_t st) {
+    if (bands <= 0) return;
+    if (P.value_symmetric) A.au = A.al;
+    dev::k_windowed<T><<<bands, dev::kWarpsPerCta * 32, P.win_smem, st>>>(A);
+}
+
+void rec(const Plan& P, int i, cudaStream_t st) {
+    if (P.timing) CUDA_OK(cudaEventRecord(P.ev[i], st));
+}
+
+template <class T>
+void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, int part) {
+    const T* x = static_cast<const T*>(dx);
+    T* y = static_cast<T*>(dy);
+    const size_t ybytes = static_cast<size_t>(P.vec_len()) * sizeof(T);
+    if (part >= 0) {
+        // band plan partial products
+        if (part == 0) CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+        auto A = win_args<T>(P, dx, dy, tr);
+        A.tile_start = P.tile_part[part].as<int32_t>();
+        A.band_tile = P.band_tile_part[part].as<int32_t>();
+        launch_windowed<T>(P, A, P.bands_part[part], st);
+        CUDA_OK(cudaGetLastError());
+        return;
+    }
+    rec(P, 0, st);
+    switch (P.exec_kind) {
+        case CSRC_KIND_WINDOWED: {
+            CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+            rec(P, 1, st);
+            launch_windowed<T>(P, win_args<T>(P, dx, dy, tr), P.bands, st);
+            rec(P, 2, st);
+            break;
+        }
+        case CSRC_KIND_ATOMIC: {
+            CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+            rec(P, 1, st);
+            launch_atomic<T>(P, tr, x, y, st);
+            rec(P, 2, st);
+            break;
+        }
+        case CSRC_KIND_COLORFUL: {
+            CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+            rec(P, 1, st);
+            launch_colored<T>(P, tr, x, y, st);
+            rec(P, 2, st);
+            break;
+        }
+        case CSRC_KIND_LOCAL_BUFFERS: {
+            auto B = buf_args<T>(P);
+            const int sms = num_sms(P.device);
+            switch (P.accum) {
+                case CSRC_ACCUM_ALL_IN_ONE:
+                    dev::k_init_flat<T><<<grid_for(P.device, P.buf_total, 256), 256, 0, st>>>(
+                        B.buf, P.buf_total);
+                    break;
+                case CSRC_ACCUM_PER_BUFFER:
+                case CSRC_ACCUM_EFFECTIVE: {
+                    dim3 g(std::max(1, sms * 4 / std::max(1, P.bands)), std::min(P.bands, 65535));
+                    dev::k_init_per_buffer<T><<<g, 256, 0, st>>>(B);
+                    break;
+                }
+                default: {
+                    dim3 g(std::max(1, sms * 4 / std::max(1, P.n_iv)),
+                           std::min(std::max(P.n_iv, 1), 65535));
+                    dev::k_init_interval<T><<<g, 256, 0, st>>>(B);
+                }
+            }
+            rec(P, 1, st);
+            auto A = win_args<T>(P, dx, P.buf.p, tr);
+            A.band_shift = P.band_shift.as<int64_t>();
+            launch_windowed<T>(P, A, P.bands, st);
+            rec(P, 2, st);
+            const int64_t shift = -static_cast<int64_t>(P.lo);
+            switch (P.accum) {
+                case CSRC_ACCUM_ALL_IN_ONE:
+                case CSRC_ACCUM_PER_BUFFER:
+                    dev::k_accum_sliced<T><<<grid_for(P.device, P.nrows, 256), 256, 0, st>>>(
+                        B, y, P.row_begin, P.row_end, shift);
+                    break;
+                case CSRC_ACCUM_EFFECTIVE: {
+                    dim3 g(std::max(1, sms * 4 / std::max(1, P.bands)), std::min(P.bands, 65535));
+                    dev::k_accum_effective<T><<<g, 256, 0, st>>>(B, y, shift);
+                    break;
+                }
+                default: {
+                    dim3 g(std::max(1, sms * 4 / std::max(1, P.n_iv)),
+                           std::min(std::max(P.n_iv, 1), 65535));
+                    dev::k_accum_interval<T><<<g, 256, 0, st>>>(B, y, shift);
+                }
+            }
+            break;
+        }
+        default:
+            throw Error("unknown strategy kind");
+    }
+    rec(P, 3, st);
+    P.ev_recorded = P.timing;
+    CUDA_OK(cudaGetLastError());
+}
+
+void apply_device(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, int part = -1) {
+    if (P.nrows == 0) return;
+    CUDA_OK(cudaSetDevice(P.device));
+    if (P.dtype == CSRC_DTYPE_F64)
+        apply_typed<double>(P, dx, dy, st, tr, part);
+    else
+        apply_typed<float>(P, dx, dy, st, tr, part);
+}
+
+void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
+    if (x_len != P.n_global)
+        throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +
+                    std::to_string(P.n_global));
+    if (P.row_begin != 0 || P.row_end != P.n_global)
+        throw Error("host products need a full-matrix plan (use the device entry points for bands)");
+    if (P.n_global == 0) return;
+    CUDA_OK(cudaSetDevice(P.device));
+    const size_t n = static_cast<size_t>(P.n_global);
+    if (!P.dx.p) P.dx.alloc(n * P.vsize());
+    if (!P.dy.p) P.dy.alloc(n * P.vsize());
+    cudaStream_t st = P.stream;
+    if (P.dtype == CSRC_DTYPE_F64) {
+        CUDA_OK(cudaMemcpyAsync(P.dx.p, xh, n * 8, cudaMemcpyHostToDevice, st));
+        apply_device(P, P.dx.p, P.dy.p, st, tr);
+        CUDA_OK(cudaMemcpyAsync(yh, P.dy.p, n * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+        if (!P.dxd.p) P.dxd.alloc(n * 8);
+        if (!P.dyd.p) P.dyd.alloc(n * 8);
+        CUDA_OK(cudaMemcpyAsync(P.dxd.p, xh, n * 8, cudaMemcpyHostToDevice, st));
+        dev::k_convert<double, float><<<grid_for(P.device, n, 256), 256, 0, st>>>(
+            P.dxd.as<double>(), P.dx.as<float>(), n);
+        apply_device(P, P.dx.p, P.dy.p, st, tr);
+        dev::k_convert<float, double><<<grid_for(P.device, n, 256), 256, 0, st>>>(
+            P.dy.as<float>(), P.dyd.as<double>(), n);
+        CUDA_OK(cudaMemcpyAsync(yh, P.dyd.p, n * 8, cudaMemcpyDeviceToHost, st));
+    }
+    CUDA_OK(cudaStreamSynchronize(st));
+}
+
+Plan* checked(csrc_gpu_plan_t p) {
+    if (!p) throw Error("null plan");
+    return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int csrc_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int csrc_gpu_plan_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
+                         csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out) throw Error("null output");
+        *out = nullptr;
+        *out = create_plan(a, s, CreateOpts{});
+    });
+}
+
+int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
+                                 const int32_t* color, int32_t n_colors, csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out || !color) throw Error("null argument");
+        *out = nullptr;
+        CreateOpts o;
+        o.color = color;
+        o.n_colors = n_colors;
+        *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_create_partitioned(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
+                                     const int32_t* block_start, int32_t bands,
+                                     csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out || !block_start) throw Error("null argument");
+        *out = nullptr;
+        CreateOpts o;
+        o.block_start = block_start;
+        o.bands = bands;
+        *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_create_band(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
+                              int32_t row_begin, int32_t row_end, csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out) throw Error("null output");
+        *out = nullptr;
+        CreateOpts o;
+        o.band = true;
+        o.row_begin = row_begin;
+        o.row_end = row_end;
+        *out = create_plan(a, s, o);
+    });
+}
+
+void csrc_gpu_plan_destroy(csrc_gpu_plan_t plan) {
+    if (plan) {
+        cudaSetDevice(plan->device);
+        cudaStreamSynchronize(plan->stream);
+        delete plan;
+    }
+}
+
+int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (!info) throw Error("null info");
+        std::memset(info, 0, sizeof(*info));
+        info->n = P.n_global;
+        info->k = P.k;
+        info->kind = P.exec_kind;
+        info->dtype = P.dtype;
+        info->bands = P.bands;
+        info->buffers_allocated = P.exec_kind == CSRC_KIND_LOCAL_BUFFERS ? P.bands : 0;
+        info->n_colors = P.n_colors;
+        info->row_begin = P.row_begin;
+        info->row_end = P.row_end;
+        info->lo = P.lo;
+        const count_t band_nnz = P.nrows + (P.value_symmetric ? 1 : 2) * P.k;
+        info->model_bytes =
+            csrc_model_bytes(P.nrows, band_nnz, P.value_symmetric ? 1 : 0, P.dtype);
+        size_t dbytes = 0;
+        for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.tile_start, &P.band_tile,
+                                &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
+                                &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.dx, &P.dy, &P.dxd, &P.dyd})
+            if (d->p) dbytes += d->bytes;
+        info->device_bytes = static_cast<int64_t>(dbytes);
+        info->near_depth = P.near_depth;
+        info->far_lo = P.far_lo;
+        info->far_hi = P.far_hi;
+        info->launches_per_apply = P.launches;
+        info->captured_fraction = P.captured;
+    });
+}
+
+int csrc_gpu_spmv(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, double* y_host) {
+    return guarded([&] { apply_host(*checked(plan), x_host, x_len, y_host, false); });
+}
+
+int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len,
+                            double* y_host) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (x_len != P.n_global)
+            throw Error("spmv_csrc_transpose: x has length " + std::to_string(x_len) +
+                        ", expected " + std::to_string(P.n_global));
+        apply_host(P, x_host, x_len, y_host, !P.value_symmetric);
+    });
+}
+
+int csrc_gpu_spmv_device(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream,
+                         int32_t flags) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
+        apply_device(P, d_x, d_y, st, (flags & 1) && !P.value_symmetric);
+    });
+}
+
+int csrc_gpu_spmv_device_graph(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
+        CUDA_OK(cudaSetDevice(P.device));
+        if (!P.graph || P.g_x != d_x || P.g_y != d_y || P.g_stream != st) {
+            if (P.graph) cudaGraphExecDestroy(P.graph);
+            P.graph = nullptr;
+            const bool was_timing = P.timing;
+            P.timing = false;
+            cudaGraph_t g;
+            CUDA_OK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            try {
+                apply_device(P, d_x, d_y, st, false);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                P.timing = was_timing;
+                throw;
+            }
+            CUDA_OK(cudaStreamEndCapture(st, &g));
+            P.timing = was_timing;
+            CUDA_OK(cudaGraphInstantiate(&P.graph, g, 0));
+            cudaGraphDestroy(g);
+            P.g_x = d_x;
+            P.g_y = d_y;
+            P.g_stream = st;
+        }
+        CUDA_OK(cudaGraphLaunch(P.graph, st));
+    });
+}
+
+int csrc_gpu_halo_accumulate(csrc_gpu_plan_t plan, void* d_y, int64_t dst_off,
+                             const void* d_recv, int64_t len, void* stream) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (len <= 0) return;
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
+        CUDA_OK(cudaSetDevice(P.device));
+        if (P.dtype == CSRC_DTYPE_F64)
+            dev::k_halo_add<double><<<grid_for(P.device, len, 256), 256, 0, st>>>(
+                static_cast<double*>(d_y) + dst_off, static_cast<const double*>(d_recv), len);
+        else
+            dev::k_halo_add<float><<<grid_for(P.device, len, 256), 256, 0, st>>>(
+                static_cast<float*>(d_y) + dst_off, static_cast<const float*>(d_recv), len);
+        CUDA_OK(cudaGetLastError());
+    });
+}
+
+int csrc_gpu_band_split(csrc_gpu_plan_t plan, int32_t* boundary_rows_end) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        *boundary_rows_end = P.split;
+    });
+}
+
+int csrc_gpu_spmv_device_part(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream,
+                              int32_t part) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (part != 0 && part != 1) throw Error("part must be 0 (boundary) or 1 (interior)");
+        if (P.row_begin == 0 && P.row_end == P.n_global)
+            throw Error("partial products need a band plan");
+        if (P.exec_kind != CSRC_KIND_WINDOWED)
+            throw Error("partial products need the windowed kernel");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
+        apply_device(P, d_x, d_y, st, false, part);
+    });
+}
+
+int csrc_gpu_set_timing(csrc_gpu_plan_t plan, int32_t enabled) {
+    return guarded([&] { checked(plan)->timing = enabled != 0; });
+}
+
+int csrc_gpu_last_timings(csrc_gpu_plan_t plan, csrc_gpu_timings* t) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        std::memset(t, 0, sizeof(*t));
+        if (!P.ev_recorded) return;
+        CUDA_OK(cudaEventSynchronize(P.ev[3]));
+        float a = 0, b = 0, c = 0;
+        CUDA_OK(cudaEventElapsedTime(&a, P.ev[0], P.ev[1]));
+        CUDA_OK(cudaEventElapsedTime(&b, P.ev[1], P.ev[2]));
+        CUDA_OK(cudaEventElapsedTime(&c, P.ev[2], P.ev[3]));
+        t->init_ms = a;
+        t->compute_ms = b;
+        t->accumulate_ms = c;
+    });
+}
+
+int csrc_gpu_time_products(csrc_gpu_plan_t plan, const void* d_x, void* d_y, int32_t reps,
+                           int64_t flush_bytes, double* ms_out, double* kernel_ms_out) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (reps < 1) throw Error("reps must be >= 1");
+        CUDA_OK(cudaSetDevice(P.device));
+        if (flush_bytes > 0 && P.flushbuf.bytes < static_cast<size_t>(flush_bytes))
+            P.flushbuf.alloc(static_cast<size_t>(flush_bytes));
+        const bool was = P.timing;
+        P.timing = true;
+        cudaStream_t st = P.stream;
+        try {
+            CUDA_OK(cudaStreamSynchronize(st));
+            for (int r = 0; r < reps; ++r) {
+                if (flush_bytes > 0)
+                    CUDA_OK(cudaMemsetAsync(P.flushbuf.p, r & 0xff, flush_bytes, st));
+                apply_device(P, d_x, d_y, st, false);
+                float tot = 0, ker = 0;
+                CUDA_OK(cudaEventSynchronize(P.ev[3]));
+                CUDA_OK(cudaEventElapsedTime(&tot, P.ev[0], P.ev[3]));
+                CUDA_OK(cudaEventElapsedTime(&ker, P.ev[1], P.ev[2]));
+                ms_out[r] = tot;
+                if (kernel_ms_out) kernel_ms_out[r] = ker;
+            }
+        } catch (...) {
+            P.timing = was;
+            throw;
+        }
+        P.timing = was;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+// sm_100a kernels for the CSRC product y = A x (reference: spmv_csrc,
+// kernels.hpp:25-43). Every kernel streams the CSRC arrays once, coalesced;
+// they differ in how the transposed scatter y[ja[t]] += au[t] * x[i] is made
+// race-free (parallel.hpp:286-435 re-derived for the GPU):
+//
+//   k_atomic    global-atomic baseline: every scatter is a red.global.add
+//   k_colored   one launch per conflict-free row class, plain read-add-write
+//   k_windowed  CTA row bands; scatters land in two shared-memory rings
+//               (near: distance <= Dn, far: distance in [Fmin, Fmax]) that
+//               slide with the tile and are flushed with coalesced
+//               red.global.add; the rest spills straight to red.global
+//
+// Positions are global row/column ids; vectors x and out are indexed
+// q + shift (shift = -lo for the device vectors covering [lo, row_end)).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace csrcgpu {
+namespace dev {
+
+constexpr int kTileRows = 512;        // rows per windowed tile (<= 65535 for u16 rowid)
+constexpr int kWarpsPerCta = 8;       // windowed CTA = 256 threads
+
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) {
+    return __ldcs(p);  // evict-first: matrix arrays are touched exactly once
+}
+
+template <typename T>
+__device__ __forceinline__ void red_add(T* p, T v) {
+    atomicAdd(p, v);  // result unused -> RED.E.ADD.{F64,F32}
+}
+
+// ----------------------------------------------------------------- atomic
+// L lanes per row; lanes stride over the row's pairs (coalesced within the
+// row segment); the row sum is a shuffle reduction; both the row result and
+// every transposed entry go through red.global.add into a zeroed y.
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_atomic(const int32_t* __restrict__ ia,
+                                                const int32_t* __restrict__ ja,
+                                                const T* __restrict__ al,
+                                                const T* __restrict__ au,
+                                                const T* __restrict__ ad,
+                                                const T* __restrict__ x, T* y, int32_t nrows,
+                                                int32_t row_begin, int64_t shift) {
+    const int sub = threadIdx.x % L;
+    const int64_t group = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+    const int64_t ngroups = static_cast<int64_t>(gridDim.x) * blockDim.x / L;
+    for (int64_t r = group; r < nrows; r += ngroups) {
+        const int64_t g = row_begin + r;
+        const T xi = __ldg(x + g + shift);
+        T s = T(0);
+        const int32_t t1 = __ldg(ia + r + 1);
+        for (int32_t t = __ldg(ia + r) + sub; t < t1; t += L) {
+            const int32_t j = ldg_stream(ja + t);
+            const T a_l = ldg_stream(al + t);
+            const T a_u = au == al ? a_l : ldg_stream(au + t);
+            s += a_l * __ldg(x + j + shift);
+            red_add(y + j + shift, a_u * xi);
+        }
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
+        if (sub == 0) red_add(y + g + shift, s + __ldg(ad + r) * xi);
+    }
+}
+
+// ---------------------------------------------------------------- colored
+// One class per launch (colorful_worker, parallel.hpp:411-434): rows of a
+// class share no written y position, so y[j] += and y[i] += are plain
+// read-add-writes. The class's rows are stored class-major (row-id list
+// `rid`, row pointers `cia` into class-major ja/al/au), so each launch
+// streams a contiguous slab.
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_colored(const int32_t* __restrict__ rid,
+                                                 const int64_t* __restrict__ cia,
+                                                 const int32_t* __restrict__ ja,
+                                                 const T* __restrict__ al,
+                                                 const T* __restrict__ au,
+                                                 const T* __restrict__ ad,
+                                                 const T* __restrict__ x, T* y, int64_t c0,
+                                                 int64_t c1, int64_t shift) {
+    const int sub = threadIdx.x % L;
+    const int64_t group = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
+    const int64_t ngroups = static_cast<int64_t>(gridDim.x) * blockDim.x / L;
+    for (int64_t r = c0 + group; r < c1; r += ngroups) {
+        const int64_t g = __ldg(rid + r);
+        const T xi = __ldg(x + g + shift);
+        T s = T(0);
+        const int64_t t1 = __ldg(cia + r + 1);
+        for (int64_t t = __ldg(cia + r) + sub; t < t1; t += L) {
+            const int32_t j = ldg_stream(ja + t);
+            const T a_l = ldg_stream(al + t);
+            const T a_u = au == al ? a_l : ldg_stream(au + t);
+            s += a_l * __ldg(x + j + shift);
+            y[j + shift] += a_u * xi;
+        }
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
+        if (sub == 0) y[g + shift] += s + ldg_stream(ad + r) * xi;
+    }
+}
+
+// --------------------------------------------------------------- windowed
+template <typename T>
+struct WinArgs {
+    const int32_t* ia;        // local rows, rebased to 0
+    const int32_t* ja;        // global column ids
+    const T* al;
+    const T* au;
+    const T* ad;              // local rows
+    const T* x;               // x[q + xshift]
+    T* out;                   // out[q + shift_b]
+    const int32_t* tile_start;  // local row index per tile (+ sentinel)
+    const int32_t* band_tile;   // tiles of band b: [band_tile[b], band_tile[b+1])
+    const int64_t* band_shift;  // per-band output shift (private buffers); null = shift
+    int64_t shift;
+    int64_t xshift;
+    int32_t row_begin;        // global id of local row 0
+    int32_t near_depth;       // Dn
+    int32_t far_lo, far_hi;   // [Fmin, Fmax]; far_lo > far_hi disables the far ring
+    int32_t ring_near;        // RN (power of two)
+    int32_t ring_far;         // RF (power of two)
+    int32_t max_tile_pairs;
+};
+
+template <typename T>
+__device__ __forceinline__ void smem_add(T* p, T v) {
+    atomicAdd(p, v);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) k_windowed(WinArgs<T> A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* ringN = reinterpret_cast<T*>(smem_raw);
+    T* ringF = ringN + A.ring_near;
+    T* xs = ringF + A.ring_far;
+    int32_t* ia_s = reinterpret_cast<int32_t*>(xs + kTileRows);
+    uint16_t* rowid = reinterpret_cast<uint16_t*>(ia_s + kTileRows + 1);
+
+    const int b = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int nthreads = blockDim.x;
+    const int maskN = A.ring_near - 1;
+    const int maskF = A.ring_far - 1;
+    const bool far_on = A.far_lo <= A.far_hi;
+    const int64_t shift = A.band_shift ? A.band_shift[b] : A.shift;
+    T* out = A.out;
+
+    const int32_t tb = A.band_tile[b], te = A.band_tile[b + 1];
+    if (tb >= te) return;
+    for (int i = tid; i < A.ring_near + (far_on ? A.ring_far : 0); i += nthreads) ringN[i] = T(0);
+
+    const int64_t band_g0 = static_cast<int64_t>(A.row_begin) + A.tile_start[tb];
+    const int64_t band_g1 = static_cast<int64_t>(A.row_begin) + A.tile_start[te];
+    int64_t near_done = band_g0 - A.near_depth;  // positions below are flushed
+    int64_t far_done = band_g0 - A.far_hi;
+
+    auto flush = [&](T* ring, int mask, int64_t from, int64_t to) {
+        if (from < 0) from = 0;
+        for (int64_t q = from + tid; q < to; q += nthreads) {
+            T* slot = ring + (q & mask);
+            const T v = *slot;
+            if (v != T(0)) {
+                red_add(out + q + shift, v);
+                *slot = T(0);
+            }
+        }
+    };
+
+    for (int32_t tile = tb; tile < te; ++tile) {
+        const int32_t r0 = A.tile_start[tile], r1 = A.tile_start[tile + 1];
+        const int32_t nr = r1 - r0;
+        const int64_t g0 = static_cast<int64_t>(A.row_begin) + r0;
+        __syncthreads();  // previous tile's pair phase done (and ring zeroing)
+        // slide: positions that no row of this tile or later can reach are final
+        flush(ringN, maskN, near_done, g0 - A.near_depth);
+        near_done = g0 - A.near_depth;
+        if (far_on) {
+            flush(ringF, maskF, far_done, g0 - A.far_hi);
+            far_done = g0 - A.far_hi;
+        }
+        for (int r = tid; r <= nr; r += nthreads) ia_s[r] = __ldg(A.ia + r0 + r);
+        for (int r = tid; r < nr; r += nthreads) xs[r] = __ldg(A.x + g0 + r + A.xshift);
+        __syncthreads();
+        const int32_t p0 = ia_s[0];
+        // row ids of the tile's pairs; diagonal term into the own-row slot
+        for (int r = tid; r < nr; r += nthreads) {
+            const int32_t a0 = ia_s[r] - p0, a1 = ia_s[r + 1] - p0;
+            for (int32_t q = a0; q < a1; ++q) rowid[q] = static_cast<uint16_t>(r);
+            ringN[(g0 + r) & maskN] += ldg_stream(A.ad + r0 + r) * xs[r];
+        }
+        __syncthreads();
+        // pair phase: contiguous, coalesced pair ranges per warp
+        const int32_t np = ia_s[nr] - p0;
+        const int32_t w0 = static_cast<int32_t>(static_cast<int64_t>(np) * warp / kWarpsPerCta);
+        const int32_t w1 =
+            static_cast<int32_t>(static_cast<int64_t>(np) * (warp + 1) / kWarpsPerCta);
+        for (int32_t base = w0; base < w1; base += 32) {
+            const int32_t q = base + lane;
+            const bool active = q < w1;
+            int key = -1 - lane;
+            T gv = T(0);
+            if (active) {
+                const int64_t t = static_cast<int64_t>(p0) + q;
+                const int r = rowid[q];
+                key = r;
+                const int32_t j = ldg_stream(A.ja + t);
+                const T a_l = ldg_stream(A.al + t);
+                const T a_u = A.au == A.al ? a_l : ldg_stream(A.au + t);  // value-symmetric
+                gv = a_l * __ldg(A.x + j + A.xshift);
+                const T sv = a_u * xs[r];
+                const int64_t d = g0 + r - j;
+                if (d <= A.near_depth) {
+                    smem_add(ringN + (j & maskN), sv);
+                } else if (far_on && d >= A.far_lo && d <= A.far_hi) {
+                    smem_add(ringF + (j & maskF), sv);
+                } else {
+                    red_add(out + j + shift, sv);
+                }
+            }
+            // segmented suffix reduction of the gather products by row
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const T v2 = __shfl_down_sync(0xffffffffu, gv, off);
+                const int k2 = __shfl_down_sync(0xffffffffu, key, off);
+                if (lane + off < 32 && k2 == key) gv += v2;
+            }
+            const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+            if (active && (lane == 0 || kprev != key)) smem_add(ringN + ((g0 + key) & maskN), gv);
+        }
+    }
+    __syncthreads();
+    flush(ringN, maskN, near_done, band_g1);
+    if (far_on) flush(ringF, maskF, far_done, band_g1 - A.far_lo);
+}
+
+// ------------------------------------------------------------ small kernels
+template <typename Tin, typename Tout>
+__global__ void k_convert(const Tin* __restrict__ in, Tout* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[i] = static_cast<Tout>(in[i]);
+}
+
+template <typename T>
+__global__ void k_halo_add(T* y, const T* __restrict__ recv, int64_t len) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < len;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        red_add(y + i, recv[i]);
+}
+
+// ------------------------------------------------ local-buffers accumulation
+// Private band buffers are stored compactly over each band's effective range
+// [blo_b, bhi_b] at buf + boff[b] (parallel.hpp:254-255 keeps p dense n-vectors;
+// the GPU keeps only the reachable window, the reference's `effective` idea).
+// Coverage of y is described by the interval plan (partition.hpp:113-134).
+template <typename T>
+struct BufArgs {
+    T* buf;
+    const int64_t* boff;      // per band
+    const int32_t* blo;       // per band effective lo
+    const int32_t* bhi;       // per band effective hi
+    const int32_t* bstart;    // per band first row (global), p+1 entries
+    const int32_t* iv_begin;  // intervals
+    const int32_t* iv_end;
+    const int32_t* cptr;      // contributors
+    const int32_t* contrib;
+    int32_t n_iv;
+    int32_t p;
+    int64_t total;            // buffer elements
+};
+
+// all_in_one init (parallel.hpp:317-325): the concatenated storage as one slab
+template <typename T>
+__global__ void k_init_flat(T* buf, int64_t total) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        buf[i] = T(0);
+}
+
+// per_buffer / effective init (parallel.hpp:327-338): one CTA row per buffer
+template <typename T>
+__global__ void k_init_per_buffer(BufArgs<T> B) {
+    for (int b = blockIdx.y; b < B.p; b += gridDim.y) {
+        const int64_t len = static_cast<int64_t>(B.bhi[b]) - B.blo[b] + 1;
+        T* base = B.buf + B.boff[b];
+        for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < len;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            base[i] = T(0);
+    }
+}
+
+// interval init (parallel.hpp:339-346): per interval, its contributors' slices
+template <typename T>
+__global__ void k_init_interval(BufArgs<T> B) {
+    for (int iv = blockIdx.y; iv < B.n_iv; iv += gridDim.y) {
+        const int32_t q0 = B.iv_begin[iv], q1 = B.iv_end[iv];
+        for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
+            const int bb = B.contrib[c];
+            T* base = B.buf + B.boff[bb] - B.blo[bb];
+            for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+                 q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x)
+                base[q] = T(0);
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ int find_interval(const BufArgs<T>& B, int32_t q) {
+    int lo = 0, hi = B.n_iv;  // first interval with end > q
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (B.iv_end[mid] <= q) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// all_in_one / per_buffer accumulation (parallel.hpp:360-369): y sliced
+// evenly; every buffer covering q contributes in ascending id.
+template <typename T>
+__global__ void k_accum_sliced(BufArgs<T> B, T* y, int32_t q_begin, int32_t q_end,
+                               int64_t shift) {
+    for (int64_t q = q_begin + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+         q < q_end; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int iv = find_interval(B, static_cast<int32_t>(q));
+        T s = T(0);
+        if (iv < B.n_iv && B.iv_begin[iv] <= q) {
+            for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
+                const int bb = B.contrib[c];
+                s += B.buf[B.boff[bb] + (q - B.blo[bb])];
+            }
+        }
+        y[q + shift] = s;
+    }
+}
+
+// effective accumulation (parallel.hpp:371-382): band b sums, for its own
+// rows, the buffers whose range covers q (ascending id).
+template <typename T>
+__global__ void k_accum_effective(BufArgs<T> B, T* y, int64_t shift) {
+    for (int b = blockIdx.y; b < B.p; b += gridDim.y) {
+        const int32_t q0 = B.bstart[b], q1 = B.bstart[b + 1];
+        for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+             q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            // covering buffers of q, ascending id, from the interval plan
+            const int iv = find_interval(B, static_cast<int32_t>(q));
+            T s = T(0);
+            if (iv < B.n_iv && B.iv_begin[iv] <= q) {
+                for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
+                    const int bb = B.contrib[c];
+                    s += B.buf[B.boff[bb] + (q - B.blo[bb])];
+                }
+            }
+            y[q + shift] = s;
+        }
+    }
+}
+
+// interval accumulation (parallel.hpp:384-394)
+template <typename T>
+__global__ void k_accum_interval(BufArgs<T> B, T* y, int64_t shift) {
+    for (int iv = blockIdx.y; iv < B.n_iv; iv += gridDim.y) {
+        const int32_t q0 = B.iv_begin[iv], q1 = B.iv_end[iv];
+        const int32_t c0 = B.cptr[iv], c1 = B.cptr[iv + 1];
+        for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+             q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            T s = T(0);
+            for (int32_t c = c0; c < c1; ++c) {
+                const int bb = B.contrib[c];
+                s += B.buf[B.boff[bb] + (q - B.blo[bb])];
+            }
+            y[q + shift] = s;
+        }
+    }
+}
+
+}  // namespace dev
+}  // namespace csrcgpu
