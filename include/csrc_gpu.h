@@ -121,10 +121,13 @@ typedef struct {
     int32_t lo;                 /* effective_range lo of the owned rows           */
     int64_t model_bytes;        /* working_set model bytes (working_set.hpp:17-25) */
     int64_t device_bytes;       /* device memory held by the plan                 */
-    int32_t near_depth;         /* windowed: near ring depth Dn                   */
-    int32_t far_lo, far_hi;     /* windowed: far ring distance window [Fmin,Fmax] */
+    int32_t n_windows;          /* windowed: scatter-distance windows             */
+    int32_t win_lo[6], win_hi[6]; /* windowed: distance interval of each window   */
+    int32_t lanes;              /* windowed: lanes per row                        */
+    int32_t stages;             /* windowed: TMA pipeline depth                   */
+    int32_t smem_bytes;         /* windowed: dynamic shared memory per CTA        */
     int32_t launches_per_apply; /* kernels launched per product                   */
-    double  captured_fraction;  /* windowed: pairs whose scatter lands in a ring  */
+    double  captured_fraction;  /* windowed: pairs whose scatter lands in a window */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;

@@ -72,9 +72,12 @@ class PlanInfo(C.Structure):
         ("lo", i32),
         ("model_bytes", i64),
         ("device_bytes", i64),
-        ("near_depth", i32),
-        ("far_lo", i32),
-        ("far_hi", i32),
+        ("n_windows", i32),
+        ("win_lo", i32 * 6),
+        ("win_hi", i32 * 6),
+        ("lanes", i32),
+        ("stages", i32),
+        ("smem_bytes", i32),
         ("launches_per_apply", i32),
         ("captured_fraction", f64),
     ]

@@ -6,6 +6,7 @@
 // init / compute / accumulate phases and records PhaseTimings-style events.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -52,17 +53,18 @@ void upload(DevBuf& d, const U* h, size_t count) {
     if (count) CUDA_OK(cudaMemcpy(d.p, h, count * sizeof(U), cudaMemcpyHostToDevice));
 }
 
+int pow2_at_least(int64_t v) {
+    int64_t p = 1;
+    while (p < v) p <<= 1;
+    return static_cast<int>(p);
+}
+
 int num_sms(int device) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
     return v > 0 ? v : 148;
 }
 
-int pow2_at_least(int64_t v) {
-    int64_t p = 1;
-    while (p < v) p <<= 1;
-    return static_cast<int>(p);
-}
 
 }  // namespace
 
@@ -85,16 +87,21 @@ struct csrc_gpu_plan_s {
     DevBuf ia, ja, al, au, ad;  // matrix (dtype values)
 
     // windowed / local buffers
-    int bands = 0;
-    DevBuf tile_start, band_tile, band_shift;
-    int near_depth = 0, far_lo = 1, far_hi = 0, ring_near = 1, ring_far = 1;
-    int max_tile_pairs = 8192;
+    int bands = 0;         // windowed CTAs (= private bands for local buffers)
+    DevBuf band_shift, sched, cta_ptr;  // sched: TileDesc per scheduled tile
+    int n_tiles = 0;
+    int near_depth = 0, far_lo = 1, far_hi = 0, ring_near = 1, ring_far = 0;
+    int max_tile_pairs = 16;
     size_t win_smem = 0;
+    int win_lanes = 1;     // L lanes per row in the windowed kernel
+    int stages = 2;
+    int stage_bytes = 0;
     double captured = 0.0;
+    std::vector<index_t> band_rows;
     // band plans: boundary / interior sub-schedules
     index_t split = 0;
     int bands_part[2] = {0, 0};
-    DevBuf tile_part[2], band_tile_part[2];
+    DevBuf sched_part[2], cta_ptr_part[2];
 
     // local buffers
     DevBuf buf, boff, blo, bhi, bstart, iv_begin, iv_end, cptr, contrib;
@@ -149,8 +156,10 @@ void upload_values(DevBuf& d, const double* h, size_t count) {
 }
 
 // --------------------------------------------------- windowed schedule
-// Ring windows from the histogram of scatter distances d = row - ja:
-// near covers 1..Dn (plus the own row), far the densest window beyond Dn.
+// Ring windows from the histogram of scatter distances d = row - ja: the
+// near ring covers 1..Dn (plus the own row), the far ring the densest
+// distance window beyond Dn; the rest spills to red.global.add. Rings hold
+// the window plus two tiles (see windowed.cuh).
 void choose_windows(Plan& P, const MatView& a) {
     const int T = dev::kTileRows;
     const int kRingMax = 2048;
@@ -161,7 +170,7 @@ void choose_windows(Plan& P, const MatView& a) {
     for (index_t r = P.row_begin; r < P.row_end; ++r)
         for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) ++hist[r - a.ja[t]];
     const count_t total = a.ia[P.row_end] - a.ia[P.row_begin];
-    int dn_cap = kRingMax - T;
+    const int dn_cap = kRingMax - 2 * T;
     int dn = 0;
     count_t near_cnt = 0;
     for (count_t d = 1; d <= std::min<count_t>(maxd, dn_cap); ++d)
@@ -170,31 +179,29 @@ void choose_windows(Plan& P, const MatView& a) {
             near_cnt += hist[d];
         }
     P.near_depth = dn;
-    P.ring_near = pow2_at_least(dn + T);
+    P.ring_near = pow2_at_least(dn + 2 * T);
     P.far_lo = 1;
     P.far_hi = 0;
-    P.ring_far = 1;
+    P.ring_far = 0;
     count_t far_cnt = 0;
     if (maxd > dn) {
-        const int W = kRingMax - T;  // window width in distances
-        count_t best = 0, cur = 0;
-        count_t best_lo = dn + 1;
-        count_t lo = dn + 1;
+        const int W = kRingMax - 2 * T;  // far window width in distances
+        count_t best = 0, cur = 0, best_lo = dn + 1, lo = dn + 1;
         for (count_t hi = dn + 1; hi <= maxd; ++hi) {
             cur += hist[hi];
-            while (hi - lo > W) cur -= hist[lo++];
+            while (hi - lo >= W) cur -= hist[lo++];
             if (cur > best) {
                 best = cur;
                 best_lo = lo;
             }
         }
         if (best > 0 && best * 50 >= total) {  // worth a ring if >= 2% of pairs
-            count_t f0 = best_lo, f1 = std::min<count_t>(best_lo + W, maxd);
+            count_t f0 = best_lo, f1 = std::min<count_t>(best_lo + W - 1, maxd);
             while (f0 < f1 && hist[f0] == 0) ++f0;
             while (f1 > f0 && hist[f1] == 0) --f1;
             P.far_lo = static_cast<int>(f0);
             P.far_hi = static_cast<int>(f1);
-            P.ring_far = pow2_at_least(f1 - f0 + 1 + T);
+            P.ring_far = pow2_at_least(f1 - f0 + 1 + 2 * T);
             far_cnt = best;
         }
     }
@@ -202,54 +209,105 @@ void choose_windows(Plan& P, const MatView& a) {
 }
 
 // Tiles (<= kTileRows rows, <= max_tile_pairs pairs) over bands given as
-// local row starts bs[0..nb].
-void build_tiles(Plan& P, const MatView& a, const std::vector<index_t>& bs, DevBuf& d_tiles,
-                 DevBuf& d_band_tile) {
-    std::vector<int32_t> tiles, band_tile;
+// local row starts bs[0..nb]; band_first[b] = first tile of band b.
+std::vector<int32_t> make_tiles(const Plan& P, const MatView& a, const std::vector<index_t>& bs,
+                                std::vector<int32_t>& band_first) {
+    std::vector<int32_t> tiles;
+    band_first.clear();
     const int nb = static_cast<int>(bs.size()) - 1;
+    const index_t g = P.row_begin;
     for (int b = 0; b < nb; ++b) {
-        band_tile.push_back(static_cast<int32_t>(tiles.size()));
+        band_first.push_back(static_cast<int32_t>(tiles.size()));
         index_t r = bs[b];
         const index_t e = bs[b + 1];
         while (r < e) {
             tiles.push_back(r);
-            index_t end = std::min<index_t>(r + dev::kTileRows, e);
-            const index_t g = P.row_begin;
-            while (end > r + 1 &&
-                   static_cast<count_t>(a.ia[g + end]) - a.ia[g + r] > P.max_tile_pairs) {
-                end = r + 1 + (end - r - 1) / 2;
-            }
-            // grow back greedily after the halving overshoot
-            while (end < std::min<index_t>(r + dev::kTileRows, e) &&
+            const index_t lim = std::min<index_t>(r + dev::kTileRows, e);
+            index_t end = r + 1;  // grow while the pair budget holds
+            while (end < lim &&
                    static_cast<count_t>(a.ia[g + end + 1]) - a.ia[g + r] <= P.max_tile_pairs)
                 ++end;
             r = end;
         }
     }
-    band_tile.push_back(static_cast<int32_t>(tiles.size()));
-    tiles.push_back(bs[nb]);
-    upload(d_tiles, tiles.data(), tiles.size());
-    upload(d_band_tile, band_tile.data(), band_tile.size());
+    band_first.push_back(static_cast<int32_t>(tiles.size()));
+    tiles.push_back(bs.empty() ? 0 : bs[nb]);
+    return tiles;
+}
+
+// CTA schedule over tiles: run_len == 0 -> band b (tiles band_first[b]..) is
+// CTA b's single run; else runs of run_len consecutive tiles dealt
+// round-robin over `ctas` CTAs. Uploaded as per-tile descriptors.
+void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_t>& tiles,
+                   const std::vector<int32_t>& band_first, int run_len, int ctas,
+                   DevBuf& d_desc, DevBuf& d_cta_ptr) {
+    const int n_tiles = static_cast<int>(tiles.size()) - 1;
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> per(static_cast<size_t>(std::max(ctas, 1)));
+    auto add_run = [&](int cta, int t0, int t1) {
+        for (int t = t0; t < t1; ++t) {
+            int32_t flags = (t == t0 ? dev::kRunStart : 0) | (t + 1 == t1 ? dev::kRunEnd : 0);
+            per[cta].push_back({t, flags});
+        }
+    };
+    if (run_len <= 0) {
+        for (size_t b = 0; b + 1 < band_first.size(); ++b)
+            if (band_first[b + 1] > band_first[b]) add_run(static_cast<int>(b), band_first[b], band_first[b + 1]);
+    } else {
+        const int n_runs = (n_tiles + run_len - 1) / run_len;
+        for (int k = 0; k < n_runs; ++k)
+            add_run(k % ctas, k * run_len, std::min(n_tiles, (k + 1) * run_len));
+    }
+    std::vector<dev::TileDesc> desc;
+    std::vector<int32_t> ptr = {0};
+    for (auto& v : per) {
+        for (auto [t, flags] : v) {
+            const int32_t r0 = tiles[t], r1 = tiles[t + 1];
+            if (r0 > dev::kRowMask) throw Error("windowed: too many rows for the tile descriptor");
+            dev::TileDesc d;
+            d.r0 = r0 | flags;
+            d.r1 = r1;
+            d.p0 = a.ia[row_begin + r0] - a.ia[row_begin];
+            d.p1 = a.ia[row_begin + r1] - a.ia[row_begin];
+            desc.push_back(d);
+        }
+        ptr.push_back(static_cast<int32_t>(desc.size()));
+    }
+    upload(d_desc, desc.data(), desc.size());
+    upload(d_cta_ptr, ptr.data(), ptr.size());
 }
 
 template <class T>
-size_t windowed_smem(const Plan& P) {
-    const bool far_on = P.far_lo <= P.far_hi;
-    size_t s = sizeof(T) * (P.ring_near + (far_on ? P.ring_far : 0) + dev::kTileRows);
-    s += sizeof(int32_t) * (dev::kTileRows + 1);
-    s += sizeof(uint16_t) * P.max_tile_pairs;
-    return (s + 15) & ~size_t(15);
+dev::StageLayout<T> stage_layout(const Plan& P) {
+    const int xn = P.near_depth + dev::kTileRows;
+    const int xf = P.far_lo <= P.far_hi ? (P.far_hi - P.far_lo) + dev::kTileRows : 0;
+    return dev::StageLayout<T>(P.max_tile_pairs, xn, xf);
 }
 
 template <class T>
-int windowed_blocks_per_sm(const Plan& P) {
-    cudaFuncSetAttribute(dev::k_windowed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(P.win_smem));
+size_t windowed_smem(const Plan& P, int stages) {
+    size_t s = static_cast<size_t>(stages) * stage_layout<T>(P).bytes;
+    s += sizeof(T) * (P.ring_near + P.ring_far);
+    return (s + 127) & ~size_t(127);
+}
+
+template <class T>
+auto windowed_fn(int L) {
+    switch (L) {
+        case 1: return dev::k_windowed<T, 1>;
+        case 2: return dev::k_windowed<T, 2>;
+        case 4: return dev::k_windowed<T, 4>;
+        default: return dev::k_windowed<T, 8>;
+    }
+}
+
+template <class T>
+int windowed_blocks_per_sm(const Plan& P, size_t smem) {
+    auto fn = windowed_fn<T>(P.win_lanes);
+    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
     int nb = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dev::k_windowed<T>,
-                                                         dev::kWarpsPerCta * 32, P.win_smem));
-    if (nb < 1) throw Error("windowed kernel does not fit on an SM (smem " +
-                            std::to_string(P.win_smem) + " B)");
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, dev::kTileRows * P.win_lanes,
+                                                         smem));
     return nb;
 }
 
@@ -262,32 +320,77 @@ MatView local_view(const MatView& a, index_t r0, index_t r1) {
     return v;
 }
 
+int pick_win_lanes(count_t k, index_t n) {
+    // measured on B200 (profiles/r01_sweep*.txt): ~6 pairs per lane is best
+    const double avg = n ? static_cast<double>(k) / n : 0.0;
+    if (avg <= 6) return 1;
+    if (avg <= 16) return 2;
+    if (avg <= 48) return 4;
+    return 8;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);  // tuning knobs for sweeps
+    return e ? std::atoi(e) : dflt;
+}
+
 template <class T>
 void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
-                    int requested_bands) {
+                    int requested_bands, bool banded) {
+    P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows));
+    if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4 && P.win_lanes != 8)
+        throw Error("windowed lanes per row must be 1, 2, 4 or 8");
     choose_windows(P, a);
+    const int rows_per_tile = dev::kTileRows;
     count_t max_row = 0;
     for (index_t r = P.row_begin; r < P.row_end; ++r)
         max_row = std::max<count_t>(max_row, a.ia[r + 1] - a.ia[r]);
-    P.max_tile_pairs = static_cast<int>(std::max<count_t>(8192, max_row));
-    if (P.max_tile_pairs > 65536) P.max_tile_pairs = static_cast<int>(max_row);
-    P.win_smem = windowed_smem<T>(P);
-    if (P.win_smem > 227 * 1024)
+    const double avg = P.nrows ? static_cast<double>(P.k) / P.nrows : 0.0;
+    count_t cap = std::min<count_t>(4096, rows_per_tile * std::max<count_t>(max_row, 1));
+    cap = std::min<count_t>(cap, static_cast<count_t>(std::ceil(rows_per_tile * avg * 1.25)) + 16);
+    P.max_tile_pairs = static_cast<int>(std::max<count_t>({cap, max_row, 16}));
+    P.stage_bytes = stage_layout<T>(P).bytes;
+    // deepest pipeline that still keeps `min_ctas` CTAs per SM
+    int per_sm = 0;
+    const int max_st = std::min(env_int("CSRC_GPU_STAGES", 4), dev::kMaxStages);
+    const int min_ctas = env_int("CSRC_GPU_MINCTAS", 2);
+    for (int st = max_st; st >= 2; --st) {
+        P.stages = st;
+        P.win_smem = windowed_smem<T>(P, st);
+        if (P.win_smem > 227 * 1024) continue;
+        per_sm = windowed_blocks_per_sm<T>(P, P.win_smem);
+        if (per_sm >= min_ctas || st == 2) break;
+    }
+    if (per_sm < 1)
         throw Error("windowed: row with " + std::to_string(max_row) +
                     " pairs exceeds the shared-memory tile budget");
-    const int per_sm = windowed_blocks_per_sm<T>(P);
+    const int resident = num_sms(P.device) * per_sm;
+    const int run_len = std::max(1, env_int("CSRC_GPU_RUN_LEN", 4));
+    std::vector<int32_t> band_first;
     std::vector<index_t> bs;
-    if (explicit_bs) {
-        bs = *explicit_bs;
+    if (banded) {
+        if (explicit_bs) {
+            bs = *explicit_bs;
+        } else {
+            int bands = requested_bands > 0 ? requested_bands : resident;
+            bands = static_cast<int>(
+                std::min<count_t>(bands, std::max<count_t>(1, P.nrows / rows_per_tile)));
+            bands = std::max(1, std::min<int>(bands, P.nrows));
+            bs = partition_by_nnz(local_view(a, P.row_begin, P.row_end), bands).block_start;
+        }
+        std::vector<int32_t> tiles = make_tiles(P, a, bs, band_first);
+        P.n_tiles = static_cast<int>(tiles.size()) - 1;
+        P.bands = static_cast<int>(bs.size()) - 1;
+        make_schedule(a, P.row_begin, tiles, band_first, 0, P.bands, P.sched, P.cta_ptr);
     } else {
-        int bands = requested_bands > 0 ? requested_bands : num_sms(P.device) * per_sm;
-        bands = static_cast<int>(std::min<count_t>(bands, std::max<count_t>(1, P.nrows / 64)));
-        bands = std::max(1, std::min<int>(bands, P.nrows));
-        RowPartition part = partition_by_nnz(local_view(a, P.row_begin, P.row_end), bands);
-        bs = part.block_start;
+        bs = {0, P.nrows};
+        std::vector<int32_t> tiles = make_tiles(P, a, bs, band_first);
+        P.n_tiles = static_cast<int>(tiles.size()) - 1;
+        const int n_runs = (P.n_tiles + run_len - 1) / run_len;
+        P.bands = std::max(1, std::min(resident, n_runs));
+        make_schedule(a, P.row_begin, tiles, band_first, run_len, P.bands, P.sched, P.cta_ptr);
     }
-    P.bands = static_cast<int>(bs.size()) - 1;
-    build_tiles(P, a, bs, P.tile_start, P.band_tile);
+    P.band_rows = bs;
     if (P.row_begin > 0 || P.row_end < P.n_global) {
         // band plan: boundary rows [row_begin, split) scatter below row_begin
         index_t split = P.row_begin;
@@ -296,20 +399,14 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
         P.split = split;
         const index_t parts[3] = {0, split - P.row_begin, P.nrows};
         for (int q = 0; q < 2; ++q) {
-            const index_t rows = parts[q + 1] - parts[q];
-            if (rows <= 0) {
-                P.bands_part[q] = 0;
-                std::vector<index_t> none = {parts[q]};
-                build_tiles(P, a, none, P.tile_part[q], P.band_tile_part[q]);
-                continue;
-            }
-            int nb = std::max(1, std::min<int>(num_sms(P.device) * per_sm,
-                                               static_cast<int>(rows / 64)));
-            RowPartition part = partition_by_nnz(
-                local_view(a, P.row_begin + parts[q], P.row_begin + parts[q + 1]), nb);
-            for (auto& v : part.block_start) v += parts[q];
-            P.bands_part[q] = nb;
-            build_tiles(P, a, part.block_start, P.tile_part[q], P.band_tile_part[q]);
+            std::vector<index_t> rng = {parts[q], parts[q + 1]};
+            if (parts[q + 1] <= parts[q]) rng = {parts[q]};
+            std::vector<int32_t> tiles = make_tiles(P, a, rng, band_first);
+            const int nt = static_cast<int>(tiles.size()) - 1;
+            const int n_runs = (nt + run_len - 1) / run_len;
+            P.bands_part[q] = std::min(resident, n_runs);
+            make_schedule(a, P.row_begin, tiles, band_first, run_len, std::max(1, P.bands_part[q]),
+                          P.sched_part[q], P.cta_ptr_part[q]);
         }
     }
 }
@@ -324,8 +421,8 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.ad = P.ad.as<T>();
     A.x = static_cast<const T*>(x);
     A.out = static_cast<T*>(out);
-    A.tile_start = P.tile_start.as<int32_t>();
-    A.band_tile = P.band_tile.as<int32_t>();
+    A.tiles = P.sched.as<dev::TileDesc>();
+    A.cta_ptr = P.cta_ptr.as<int32_t>();
     A.band_shift = nullptr;
     A.shift = -static_cast<int64_t>(P.lo);
     A.xshift = -static_cast<int64_t>(P.lo);
@@ -336,6 +433,12 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.ring_near = P.ring_near;
     A.ring_far = P.ring_far;
     A.max_tile_pairs = P.max_tile_pairs;
+    A.stages = P.stages;
+    A.stage_bytes = P.stage_bytes;
+    A.x_lo = P.lo;
+    A.x_hi = P.row_end;
+    A.xn_len = P.near_depth + dev::kTileRows;
+    A.xf_len = P.far_lo <= P.far_hi ? (P.far_hi - P.far_lo) + dev::kTileRows : 0;
     return A;
 }
 
@@ -343,14 +446,8 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
 template <class T>
 void setup_buffers(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
                    int requested_bands) {
-    setup_windowed<T>(P, a, explicit_bs, requested_bands);
-    // band starts (global) from the tiles: recompute from the schedule input
-    std::vector<int32_t> tiles(P.tile_start.bytes / 4), band_tile(P.band_tile.bytes / 4);
-    CUDA_OK(cudaMemcpy(tiles.data(), P.tile_start.p, P.tile_start.bytes, cudaMemcpyDeviceToHost));
-    CUDA_OK(cudaMemcpy(band_tile.data(), P.band_tile.p, P.band_tile.bytes,
-                       cudaMemcpyDeviceToHost));
-    std::vector<index_t> bs(P.bands + 1);
-    for (int b = 0; b <= P.bands; ++b) bs[b] = tiles[band_tile[b]];
+    setup_windowed<T>(P, a, explicit_bs, requested_bands, true);
+    const std::vector<index_t>& bs = P.band_rows;  // full plans: local == global rows
     std::vector<index_t> lo, hi;
     effective_ranges(a, bs, lo, hi);
     std::vector<int64_t> off(P.bands + 1, 0), shift(P.bands);
@@ -472,7 +569,8 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
         case CSRC_KIND_WINDOWED: {
             std::vector<index_t> bs;
             if (o.block_start) bs.assign(o.block_start, o.block_start + o.bands + 1);
-            setup_windowed<T>(P, a, o.block_start ? &bs : nullptr, s.bands);
+            setup_windowed<T>(P, a, o.block_start ? &bs : nullptr, s.bands,
+                              o.block_start != nullptr);
             P.launches = 2;
             break;
         }
@@ -637,10 +735,14 @@ void launch_colored(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
 }
 
 template <class T>
-void launch_windowed(const Plan& P, dev::WinArgs<T> A, int bands, cudaStream_t st) {
-    if (bands <= 0) return;
+void launch_windowed(const Plan& P, dev::WinArgs<T> A, int ctas, cudaStream_t st) {
+    if (ctas <= 0) return;
     if (P.value_symmetric) A.au = A.al;
-    dev::k_windowed<T><<<bands, dev::kWarpsPerCta * 32, P.win_smem, st>>>(A);
+    auto fn = windowed_fn<T>(P.win_lanes);
+    // per-plan shared-memory size: the attribute is per function, so set it per launch
+    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(P.win_smem)));
+    fn<<<ctas, dev::kTileRows * P.win_lanes, P.win_smem, st>>>(A);
 }
 
 void rec(const Plan& P, int i, cudaStream_t st) {
@@ -656,8 +758,8 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
         // band plan partial products
         if (part == 0) CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
         auto A = win_args<T>(P, dx, dy, tr);
-        A.tile_start = P.tile_part[part].as<int32_t>();
-        A.band_tile = P.band_tile_part[part].as<int32_t>();
+        A.tiles = P.sched_part[part].as<dev::TileDesc>();
+        A.cta_ptr = P.cta_ptr_part[part].as<int32_t>();
         launch_windowed<T>(P, A, P.bands_part[part], st);
         CUDA_OK(cudaGetLastError());
         return;
@@ -869,15 +971,21 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         info->model_bytes =
             csrc_model_bytes(P.nrows, band_nnz, P.value_symmetric ? 1 : 0, P.dtype);
         size_t dbytes = 0;
-        for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.tile_start, &P.band_tile,
+        for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
                                 &P.cja, &P.cal, &P.cau, &P.cad, &P.dx, &P.dy, &P.dxd, &P.dyd})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
-        info->near_depth = P.near_depth;
-        info->far_lo = P.far_lo;
-        info->far_hi = P.far_hi;
+        info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS
+                              ? (P.far_lo <= P.far_hi ? 2 : 1) : 0;
+        info->win_lo[0] = 0;
+        info->win_hi[0] = P.near_depth;
+        info->win_lo[1] = P.far_lo;
+        info->win_hi[1] = P.far_hi;
+        info->lanes = P.win_lanes;
+        info->stages = P.stages;
+        info->smem_bytes = static_cast<int32_t>(P.win_smem);
         info->launches_per_apply = P.launches;
         info->captured_fraction = P.captured;
     });

@@ -20,8 +20,6 @@
 namespace csrcgpu {
 namespace dev {
 
-constexpr int kTileRows = 512;        // rows per windowed tile (<= 65535 for u16 rowid)
-constexpr int kWarpsPerCta = 8;       // windowed CTA = 256 threads
 
 template <typename T>
 __device__ __forceinline__ T ldg_stream(const T* p) {
@@ -45,24 +43,30 @@ __global__ void __launch_bounds__(256) k_atomic(const int32_t* __restrict__ ia,
                                                 const T* __restrict__ ad,
                                                 const T* __restrict__ x, T* y, int32_t nrows,
                                                 int32_t row_begin, int64_t shift) {
+    // trip counts are uniform across the block so the width-L shuffles
+    // always see all 32 lanes of the warp
     const int sub = threadIdx.x % L;
-    const int64_t group = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
-    const int64_t ngroups = static_cast<int64_t>(gridDim.x) * blockDim.x / L;
-    for (int64_t r = group; r < nrows; r += ngroups) {
-        const int64_t g = row_begin + r;
-        const T xi = __ldg(x + g + shift);
-        T s = T(0);
-        const int32_t t1 = __ldg(ia + r + 1);
-        for (int32_t t = __ldg(ia + r) + sub; t < t1; t += L) {
-            const int32_t j = ldg_stream(ja + t);
-            const T a_l = ldg_stream(al + t);
-            const T a_u = au == al ? a_l : ldg_stream(au + t);
-            s += a_l * __ldg(x + j + shift);
-            red_add(y + j + shift, a_u * xi);
+    const int rows_per_block = blockDim.x / L;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * rows_per_block; base < nrows;
+         base += static_cast<int64_t>(gridDim.x) * rows_per_block) {
+        const int64_t r = base + threadIdx.x / L;
+        const bool act = r < nrows;
+        T s = T(0), xi = T(0);
+        if (act) {
+            const int64_t g = row_begin + r;
+            xi = __ldg(x + g + shift);
+            const int32_t t1 = __ldg(ia + r + 1);
+            for (int32_t t = __ldg(ia + r) + sub; t < t1; t += L) {
+                const int32_t j = ldg_stream(ja + t);
+                const T a_l = ldg_stream(al + t);
+                const T a_u = au == al ? a_l : ldg_stream(au + t);
+                s += a_l * __ldg(x + j + shift);
+                red_add(y + j + shift, a_u * xi);
+            }
         }
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
-        if (sub == 0) red_add(y + g + shift, s + __ldg(ad + r) * xi);
+        if (act && sub == 0) red_add(y + row_begin + r + shift, s + __ldg(ad + r) * xi);
     }
 }
 
@@ -82,161 +86,38 @@ __global__ void __launch_bounds__(256) k_colored(const int32_t* __restrict__ rid
                                                  const T* __restrict__ x, T* y, int64_t c0,
                                                  int64_t c1, int64_t shift) {
     const int sub = threadIdx.x % L;
-    const int64_t group = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / L;
-    const int64_t ngroups = static_cast<int64_t>(gridDim.x) * blockDim.x / L;
-    for (int64_t r = c0 + group; r < c1; r += ngroups) {
-        const int64_t g = __ldg(rid + r);
-        const T xi = __ldg(x + g + shift);
-        T s = T(0);
-        const int64_t t1 = __ldg(cia + r + 1);
-        for (int64_t t = __ldg(cia + r) + sub; t < t1; t += L) {
-            const int32_t j = ldg_stream(ja + t);
-            const T a_l = ldg_stream(al + t);
-            const T a_u = au == al ? a_l : ldg_stream(au + t);
-            s += a_l * __ldg(x + j + shift);
-            y[j + shift] += a_u * xi;
+    const int rows_per_block = blockDim.x / L;
+    for (int64_t base = c0 + static_cast<int64_t>(blockIdx.x) * rows_per_block; base < c1;
+         base += static_cast<int64_t>(gridDim.x) * rows_per_block) {
+        const int64_t r = base + threadIdx.x / L;
+        const bool act = r < c1;
+        T s = T(0), xi = T(0);
+        int64_t g = 0;
+        if (act) {
+            g = __ldg(rid + r);
+            xi = __ldg(x + g + shift);
+            const int64_t t1 = __ldg(cia + r + 1);
+            for (int64_t t = __ldg(cia + r) + sub; t < t1; t += L) {
+                const int32_t j = ldg_stream(ja + t);
+                const T a_l = ldg_stream(al + t);
+                const T a_u = au == al ? a_l : ldg_stream(au + t);
+                s += a_l * __ldg(x + j + shift);
+                y[j + shift] += a_u * xi;
+            }
         }
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
-        if (sub == 0) y[g + shift] += s + ldg_stream(ad + r) * xi;
+        if (act && sub == 0) y[g + shift] += s + ldg_stream(ad + r) * xi;
     }
 }
 
-// --------------------------------------------------------------- windowed
-template <typename T>
-struct WinArgs {
-    const int32_t* ia;        // local rows, rebased to 0
-    const int32_t* ja;        // global column ids
-    const T* al;
-    const T* au;
-    const T* ad;              // local rows
-    const T* x;               // x[q + xshift]
-    T* out;                   // out[q + shift_b]
-    const int32_t* tile_start;  // local row index per tile (+ sentinel)
-    const int32_t* band_tile;   // tiles of band b: [band_tile[b], band_tile[b+1])
-    const int64_t* band_shift;  // per-band output shift (private buffers); null = shift
-    int64_t shift;
-    int64_t xshift;
-    int32_t row_begin;        // global id of local row 0
-    int32_t near_depth;       // Dn
-    int32_t far_lo, far_hi;   // [Fmin, Fmax]; far_lo > far_hi disables the far ring
-    int32_t ring_near;        // RN (power of two)
-    int32_t ring_far;         // RF (power of two)
-    int32_t max_tile_pairs;
-};
+}  // namespace dev
+}  // namespace csrcgpu
 
-template <typename T>
-__device__ __forceinline__ void smem_add(T* p, T v) {
-    atomicAdd(p, v);
-}
+#include "windowed.cuh"
 
-template <typename T>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) k_windowed(WinArgs<T> A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* ringN = reinterpret_cast<T*>(smem_raw);
-    T* ringF = ringN + A.ring_near;
-    T* xs = ringF + A.ring_far;
-    int32_t* ia_s = reinterpret_cast<int32_t*>(xs + kTileRows);
-    uint16_t* rowid = reinterpret_cast<uint16_t*>(ia_s + kTileRows + 1);
-
-    const int b = blockIdx.x;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int warp = tid >> 5;
-    const int nthreads = blockDim.x;
-    const int maskN = A.ring_near - 1;
-    const int maskF = A.ring_far - 1;
-    const bool far_on = A.far_lo <= A.far_hi;
-    const int64_t shift = A.band_shift ? A.band_shift[b] : A.shift;
-    T* out = A.out;
-
-    const int32_t tb = A.band_tile[b], te = A.band_tile[b + 1];
-    if (tb >= te) return;
-    for (int i = tid; i < A.ring_near + (far_on ? A.ring_far : 0); i += nthreads) ringN[i] = T(0);
-
-    const int64_t band_g0 = static_cast<int64_t>(A.row_begin) + A.tile_start[tb];
-    const int64_t band_g1 = static_cast<int64_t>(A.row_begin) + A.tile_start[te];
-    int64_t near_done = band_g0 - A.near_depth;  // positions below are flushed
-    int64_t far_done = band_g0 - A.far_hi;
-
-    auto flush = [&](T* ring, int mask, int64_t from, int64_t to) {
-        if (from < 0) from = 0;
-        for (int64_t q = from + tid; q < to; q += nthreads) {
-            T* slot = ring + (q & mask);
-            const T v = *slot;
-            if (v != T(0)) {
-                red_add(out + q + shift, v);
-                *slot = T(0);
-            }
-        }
-    };
-
-    for (int32_t tile = tb; tile < te; ++tile) {
-        const int32_t r0 = A.tile_start[tile], r1 = A.tile_start[tile + 1];
-        const int32_t nr = r1 - r0;
-        const int64_t g0 = static_cast<int64_t>(A.row_begin) + r0;
-        __syncthreads();  // previous tile's pair phase done (and ring zeroing)
-        // slide: positions that no row of this tile or later can reach are final
-        flush(ringN, maskN, near_done, g0 - A.near_depth);
-        near_done = g0 - A.near_depth;
-        if (far_on) {
-            flush(ringF, maskF, far_done, g0 - A.far_hi);
-            far_done = g0 - A.far_hi;
-        }
-        for (int r = tid; r <= nr; r += nthreads) ia_s[r] = __ldg(A.ia + r0 + r);
-        for (int r = tid; r < nr; r += nthreads) xs[r] = __ldg(A.x + g0 + r + A.xshift);
-        __syncthreads();
-        const int32_t p0 = ia_s[0];
-        // row ids of the tile's pairs; diagonal term into the own-row slot
-        for (int r = tid; r < nr; r += nthreads) {
-            const int32_t a0 = ia_s[r] - p0, a1 = ia_s[r + 1] - p0;
-            for (int32_t q = a0; q < a1; ++q) rowid[q] = static_cast<uint16_t>(r);
-            ringN[(g0 + r) & maskN] += ldg_stream(A.ad + r0 + r) * xs[r];
-        }
-        __syncthreads();
-        // pair phase: contiguous, coalesced pair ranges per warp
-        const int32_t np = ia_s[nr] - p0;
-        const int32_t w0 = static_cast<int32_t>(static_cast<int64_t>(np) * warp / kWarpsPerCta);
-        const int32_t w1 =
-            static_cast<int32_t>(static_cast<int64_t>(np) * (warp + 1) / kWarpsPerCta);
-        for (int32_t base = w0; base < w1; base += 32) {
-            const int32_t q = base + lane;
-            const bool active = q < w1;
-            int key = -1 - lane;
-            T gv = T(0);
-            if (active) {
-                const int64_t t = static_cast<int64_t>(p0) + q;
-                const int r = rowid[q];
-                key = r;
-                const int32_t j = ldg_stream(A.ja + t);
-                const T a_l = ldg_stream(A.al + t);
-                const T a_u = A.au == A.al ? a_l : ldg_stream(A.au + t);  // value-symmetric
-                gv = a_l * __ldg(A.x + j + A.xshift);
-                const T sv = a_u * xs[r];
-                const int64_t d = g0 + r - j;
-                if (d <= A.near_depth) {
-                    smem_add(ringN + (j & maskN), sv);
-                } else if (far_on && d >= A.far_lo && d <= A.far_hi) {
-                    smem_add(ringF + (j & maskF), sv);
-                } else {
-                    red_add(out + j + shift, sv);
-                }
-            }
-            // segmented suffix reduction of the gather products by row
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const T v2 = __shfl_down_sync(0xffffffffu, gv, off);
-                const int k2 = __shfl_down_sync(0xffffffffu, key, off);
-                if (lane + off < 32 && k2 == key) gv += v2;
-            }
-            const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
-            if (active && (lane == 0 || kprev != key)) smem_add(ringN + ((g0 + key) & maskN), gv);
-        }
-    }
-    __syncthreads();
-    flush(ringN, maskN, near_done, band_g1);
-    if (far_on) flush(ringF, maskF, far_done, band_g1 - A.far_lo);
-}
+namespace csrcgpu {
+namespace dev {
 
 // ------------------------------------------------------------ small kernels
 template <typename Tin, typename Tout>

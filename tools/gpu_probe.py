@@ -11,6 +11,8 @@ kinds = [('windowed', P.StrategyKind.windowed, 0), ('atomic', P.StrategyKind.ato
          ('colorful', P.StrategyKind.colorful, 0), ('lb_effective', P.StrategyKind.local_buffers, 2),
          ('lb_interval', P.StrategyKind.local_buffers, 3), ('lb_all_in_one', P.StrategyKind.local_buffers, 0),
          ('lb_per_buffer', P.StrategyKind.local_buffers, 1)]
+only = os.environ.get('KINDS')
+if only: kinds = [k for k in kinds if k[0] in only.split(',')]
 for name in cfgs:
     t = time.time(); a, x, _ = P.config_matrix(name); tg = time.time() - t
     t = time.time(); yref = O.spmv_csrc(a, x); to = time.time() - t
@@ -31,11 +33,12 @@ for name in cfgs:
             inf = ex.info()
             hot = np.median(tot[3:]); cold = np.median(totc[2:]); kc = np.median(kerc[2:])
             print(f'  {kn:14s} err {err:.2e}/{err_d:.2e} plan {tp:.2f}s hot {hot*1e3:8.1f}us cold {cold*1e3:8.1f}us '
-                  f'(kernel {kc*1e3:8.1f}us) cold GB/s {mb/cold/1e6:7.1f} bands {inf.bands} Dn {inf.near_depth} '
-                  f'far [{inf.far_lo},{inf.far_hi}] capt {inf.captured_fraction:.3f} colors {inf.n_colors}', flush=True)
+                  f'(kernel {kc*1e3:8.1f}us) cold GB/s {mb/cold/1e6:7.1f} warps {inf.bands} L {inf.lanes} st {inf.stages} '
+                  f'smem {inf.smem_bytes} win {[(inf.win_lo[i], inf.win_hi[i]) for i in range(inf.n_windows)]} capt {inf.captured_fraction:.3f} colors {inf.n_colors}', flush=True)
             ex.close()
         except Exception as e:
             print(f'  {kn:14s} FAILED: {e}', flush=True)
+    if os.environ.get('NOF32'): continue
     # fp32 windowed
     ex = P.GpuSpmv(a, P.Strategy(P.StrategyKind.windowed, dtype=P.DType.f32))
     x32 = x.astype(np.float32).astype(np.float64)
