@@ -1,0 +1,330 @@
+"""Benchmark: CSRC SpMV GFLOP/s and effective HBM GB/s (% of roofline) on B200.
+
+One step = one product y = A x over the workload (default: BASELINE.json
+config 5, the 3D 256^3 27-point FE matrix in fp64, n = 16.8M, nnz = 449M,
+4.80 GB per product by the reference's working-set model).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--dtype f64]
+  python bench.py --impl reference ...     reference CPU implementation
+
+N > 1 runs under torchrun, one rank per GPU: rank g owns a partition_by_nnz row
+band and the halo partials travel over NCCL (paper_1003_0952_b200/dist.py).
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CSRC SpMV GFLOP/s and effective HBM GB/s (% of roofline) at 1/2/4/8 B200"
+
+
+def load_peaks():
+    for p in (os.path.join(ROOT, "MEASURED_PEAKS.json"),):
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(workload):
+    p = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(workload)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.5)  # let nvidia-smi start sampling before the timed region
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(f[1]), smax=float(f[2]), power=float(f[3]),
+                                 hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        reasons = set()
+        for r in rows:
+            if r["hw"] == "Active":
+                reasons.add("hw_slowdown")
+            if r["hwt"] == "Active":
+                reasons.add("hw_thermal_slowdown")
+            if r["swt"] == "Active":
+                reasons.add("sw_thermal_slowdown")
+            if r["pcap"] == "Active":
+                reasons.add("sw_power_cap")
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows),
+                "sm_max_mhz": max(r["smax"] for r in rows), "samples": len(rows),
+                "reasons": sorted(reasons)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference(a, x, seconds, threads, sample_reps=None):
+    """Reference CPU path timed on this host: oracle/_ref ParallelSpmv
+    (interval accumulation, p = host threads) when built, else the plain-C
+    oracle port (single thread). Returns dict(value_gflops, ...)."""
+    from oracle.oracle import Oracle, Ref
+    flops = 2 * a.nnz_full()
+    if Ref.available():
+        R = Ref()
+        h = R.exec_create(a, 1, 3, threads)  # local_buffers, interval (fastest)
+        dt1, y, _ = R.exec_run(h, x, 1, a.n)  # warm
+        reps = sample_reps or max(1, min(500, int(seconds / max(dt1, 1e-6))))
+        dt, y, ph = R.exec_run(h, x, reps, a.n)
+        R.exec_destroy(h)
+        return dict(value=flops * reps / dt / 1e9, kind="reference", cores=threads, reps=reps,
+                    seconds=dt, y=y,
+                    sample=f"{reps} products of the full workload, reference ParallelSpmv "
+                           f"(local_buffers/interval, p={threads}), oracle/_ref built from /root/reference")
+    O = Oracle()
+    t0 = time.perf_counter()
+    y = O.spmv_csrc(a, x)
+    dt1 = time.perf_counter() - t0
+    reps = sample_reps or max(1, min(200, int(seconds / max(dt1, 1e-6))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        y = O.spmv_csrc(a, x)
+    dt = time.perf_counter() - t0
+    return dict(value=flops * reps / dt / 1e9, kind="port", cores=1, reps=reps, seconds=dt, y=y,
+                sample=f"{reps} products of the full workload, plain-C oracle port of spmv_csrc (1 thread)")
+
+
+def run_reference_arm(args, world, rank):
+    if world > 1 and rank != 0:
+        return 0
+    import paper_1003_0952_b200 as P
+    a, x, _ = P.config_matrix(args.config)
+    if args.dtype == "f32":
+        a = P.CsrcMatrix(a.n, a.ad.astype(np.float32).astype(np.float64), a.ia, a.ja,
+                         a.al.astype(np.float32).astype(np.float64),
+                         a.au.astype(np.float32).astype(np.float64))
+        x = x.astype(np.float32).astype(np.float64)
+    threads = os.cpu_count() or 1
+    per_step = []
+    res = None
+    for i in range(args.warmup + args.steps):
+        res = cpu_reference(a, x, args.ref_seconds / max(args.steps, 1), threads)
+        if i >= args.warmup:
+            per_step.append(res["seconds"] / res["reps"])
+    ms = 1e3 * statistics.median(per_step)
+    flops = 2 * a.nnz_full()
+    value = flops / (ms / 1e3) / 1e9
+    mb = P.model_bytes(a, P.DType.f32 if args.dtype == "f32" else P.DType.f64)
+    line = dict(
+        metric=METRIC, value=value, unit="GFLOP/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=ms, higher_is_better=True, scaling="weak" if world > 1 else "strong",
+        vs_baseline=None, dtype=args.dtype, data="synthetic",
+        config=workload_config(args, a, world), impl="reference",
+        effective_gbs=mb / (ms / 1e3) / 1e9,
+        cpu_baseline=dict(value=value, unit="GFLOP/s", cores=res["cores"], kind=res["kind"],
+                          sample=res["sample"]),
+        e2e=dict(value=value, unit="GFLOP/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+    )
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args, a, world):
+    import paper_1003_0952_b200 as P
+    c = P.CONFIGS[args.config]
+    return {"workload": f"{args.config}: {c['desc']}, {args.dtype}", "n": a.n, "nnz": a.nnz_full(),
+            "pairs": a.k_off(), "kind": args.kind, "parallelism": f"row bands x{world}" if world > 1 else "1 GPU",
+            "l2": "working set > 126 MB L2 (no flush needed)" if P.model_bytes(a) > 400e6
+            else f"L2 flushed between steps ({args.flush_mb} MB write)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--kind", default="windowed", choices=["windowed", "atomic", "colorful", "local_buffers"])
+    ap.add_argument("--flush-mb", type=int, default=256)
+    ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import torch
+    import paper_1003_0952_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dtype = P.DType.f32 if args.dtype == "f32" else P.DType.f64
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    a, x, _ = P.config_matrix(args.config)
+    mb = P.model_bytes(a, dtype)
+    flops = 2 * a.nnz_full()
+    kind = P.StrategyKind[args.kind]
+    strat = P.Strategy(kind, P.AccumMethod.interval, p=8, dtype=dtype, device=local)
+    flush = 0 if mb > 400e6 else args.flush_mb << 20
+
+    if world == 1:
+        ex = P.GpuSpmv(a, strat)
+        xd = torch.from_numpy(x).to(device="cuda", dtype=tdt)
+        yd = torch.zeros_like(xd)
+        for _ in range(args.warmup):
+            ex.apply_device(xd, yd)
+        torch.cuda.synchronize()
+        with ClockSampler(local) as cs:
+            tot, ker = ex.time_products(xd, yd, args.steps, flush)
+            torch.cuda.synchronize()
+        clocks = cs.summary()
+        ms = float(np.mean(tot))
+        kms = float(np.mean(ker))
+        info = ex.info()
+        launches_per_step = 1 if args.kind in ("windowed", "atomic") else info.launches_per_apply
+        # end to end through the public host API: pinned x -> device, product, y -> pinned host
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        ex.apply(xh.numpy(), yh.numpy())
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            ex.apply(xh.numpy(), yh.numpy())
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        ex.close()
+        ms_max = ms
+    else:
+        from paper_1003_0952_b200.dist import DistSpmv
+        ds = DistSpmv(a, strat)
+        p = ds.plan
+        xd = torch.from_numpy(x[p.lo:p.row_end].copy()).to(device="cuda", dtype=tdt)
+        yd = torch.zeros_like(xd)
+        dist.barrier()
+        for _ in range(args.warmup):
+            ds.apply_device(xd, yd)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as cs:
+            e0.record()
+            for _ in range(args.steps):
+                ds.apply_device(xd, yd)
+            e1.record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        clocks = cs.summary()
+        ms = e0.elapsed_time(e1) / args.steps
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        kms = ms
+        launches_per_step = 3 + len(p.recvs)
+        # e2e: host slice in, owned rows out
+        xh = torch.from_numpy(x[p.lo:p.row_end].copy()).pin_memory()
+        yh = torch.empty(p.row_end - p.row_begin, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            xd.copy_(xh.to(tdt), non_blocking=True)
+            ds.apply_device(xd, yd)
+            yh.copy_(yd[p.row_begin - p.lo:].to(torch.float64), non_blocking=True)
+            torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        te = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        ds.close()
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return 0
+    peak, peak_src = load_peaks()
+    gbs = mb / (ms_max / 1e3) / 1e9
+    achieved = mb / (kms / 1e3) / 1e9
+    elem = 4 if args.dtype == "f32" else 8
+    wl = f"{args.config}-{args.dtype}-{args.kind}"
+    line = dict(
+        metric=METRIC, value=flops / (ms_max / 1e3) / 1e9, unit="GFLOP/s", n_gpus=world, steps=args.steps,
+        warmup=args.warmup, ms_per_step=ms_max, higher_is_better=True,
+        scaling="strong", vs_baseline=None, dtype=args.dtype,
+        data="synthetic (BASELINE config, seeded fixture, DESIGN.md Fixtures)",
+        config=workload_config(args, a, world),
+        effective_gbs=gbs, roofline_frac_of_measured_hbm=gbs / peak,
+        gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
+        roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+                      traffic=load_traffic(wl), peak_source=peak_src,
+                      kernel="k_windowed" if args.kind == "windowed" else args.kind,
+                      algorithmic_bytes_per_launch=mb, kernel_ms=kms),
+        e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
+                 else (p.row_end - p.lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
+                 else (p.row_end - p.row_begin) * 8, wall_ms_per_step=e2e_s * 1e3),
+        gpu_launches=launches_per_step * args.steps,
+        clocks=clocks,
+    )
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        res = cpu_reference(a if args.dtype == "f64" else a, x, 15.0, threads)
+        line["cpu_baseline"] = dict(value=res["value"], unit="GFLOP/s", cores=res["cores"], kind=res["kind"],
+                                    sample=res["sample"])
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,174 @@
+"""Multi-GPU CSRC product: one process per GPU, row bands, halo reduce.
+
+Rank g owns rows [block_start[g], block_start[g+1]) of
+``partition_by_nnz(a, world)`` (partition.hpp:55-90, bit-exact) and computes
+its band with a band plan of the windowed kernel. Because ja[t] < row(t)
+(csrc_matrix.hpp:18), a band only scatters *downward*, into
+[lo_g, block_start[g]) where lo_g is its effective_range lo
+(partition.hpp:94-102): that halo partial is shipped to the owning lower
+ranks and added there. This is the reference's `effective` accumulation
+(parallel.hpp:371-382) at GPU granularity.
+
+Per product (``apply_device``):
+  1. boundary rows (those whose scatters reach below block_start[g]) run
+     first on the compute stream; an event marks the halo complete;
+  2. the communication stream waits on that event and posts the grouped
+     ncclSend/ncclRecv of the halo slices (torch.distributed P2P over NCCL,
+     NVLink/NVSwitch on the B200 box);
+  3. the interior rows run concurrently on the compute stream;
+  4. the received partials are reduced into the owned rows with a red.global
+     kernel (csrc_gpu_halo_accumulate) once the receives complete.
+
+x is replicated over each rank's [lo_g, end_g).
+
+Host mode (``band_compute`` given, CPU tensors, gloo) runs the same exchange
+plan with an injected band product; tests/test_dist.py uses it to check the
+halo logic on CPU with world size 2.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, List, Optional, Tuple
+
+import numpy as np
+
+from . import CsrcMatrix, GpuSpmv, Strategy, StrategyKind, effective_ranges, partition_by_nnz
+
+
+@dataclass
+class HaloPlan:
+    rank: int
+    world: int
+    row_begin: int
+    row_end: int
+    lo: int
+    # (peer, q0, q1): global positions [q0, q1) of my halo owned by peer
+    sends: List[Tuple[int, int, int]]
+    # (peer, q0, q1): global positions [q0, q1) of my rows in peer's halo
+    recvs: List[Tuple[int, int, int]]
+
+    @property
+    def vec_len(self) -> int:
+        return self.row_end - self.lo
+
+    def halo_bytes(self, elem: int = 8) -> Tuple[int, int]:
+        s = sum(q1 - q0 for _, q0, q1 in self.sends) * elem
+        r = sum(q1 - q0 for _, q0, q1 in self.recvs) * elem
+        return s, r
+
+
+def halo_plan(a: CsrcMatrix, world: int, rank: int) -> HaloPlan:
+    """Exchange plan of rank `rank` (identical inputs on every rank)."""
+    part = partition_by_nnz(a, world)
+    ranges = effective_ranges(a, part)
+    r0, r1 = part.begin(rank), part.end(rank)
+    lo = ranges[rank].lo
+    sends, recvs = [], []
+    for b in range(rank):  # owners of my halo [lo, r0)
+        q0, q1 = max(lo, part.begin(b)), min(r0, part.end(b))
+        if q0 < q1:
+            sends.append((b, q0, q1))
+    for c in range(rank + 1, world):  # higher ranks whose halo covers my rows
+        q0, q1 = max(ranges[c].lo, r0), min(part.begin(c), r1)
+        if q0 < q1:
+            recvs.append((c, q0, q1))
+    return HaloPlan(rank, world, r0, r1, lo, sends, recvs)
+
+
+class DistSpmv:
+    """Band-decomposed product on the current process group.
+
+    Device mode: x_local / y_local are CUDA tensors covering global positions
+    [plan.lo, plan.row_end); after ``apply_device`` the owned rows
+    y_local[row_begin - lo:] hold the final product rows.
+    """
+
+    def __init__(self, a: CsrcMatrix, strategy: Optional[Strategy] = None, group=None,
+                 band_compute: Optional[Callable] = None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.plan = halo_plan(a, self.world, self.rank)
+        self.band_compute = band_compute
+        self.ex = None
+        if band_compute is None:
+            s = strategy or Strategy(StrategyKind.windowed)
+            self.ex = GpuSpmv(a, s, band=(self.plan.row_begin, self.plan.row_end))
+            assert self.ex.info().lo == self.plan.lo
+        self._bufs = None
+        self._streams = None
+
+    def close(self):
+        if self.ex is not None:
+            self.ex.close()
+            self.ex = None
+
+    # -------------------------------------------------------------- exchange
+    def _post(self, y_local, recv_bufs):
+        dist = self.dist
+        p = self.plan
+        ops = []
+        for peer, q0, q1 in p.sends:
+            ops.append(dist.P2POp(dist.isend, y_local[q0 - p.lo:q1 - p.lo], peer, self.group))
+        for (peer, q0, q1), buf in zip(p.recvs, recv_bufs):
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def apply_host(self, x_local, y_local):
+        """Host mode (gloo): band product via the injected callable."""
+        import torch
+
+        p = self.plan
+        y_local.copy_(torch.as_tensor(self.band_compute(p, x_local.numpy())))
+        recv_bufs = [torch.empty(q1 - q0, dtype=y_local.dtype) for _, q0, q1 in p.recvs]
+        for w in self._post(y_local, recv_bufs):
+            w.wait()
+        for (peer, q0, q1), buf in zip(p.recvs, recv_bufs):
+            y_local[q0 - p.lo:q1 - p.lo] += buf
+        return y_local
+
+    def apply_device(self, x_local, y_local, overlap: bool = True):
+        import torch
+
+        p = self.plan
+        if self._streams is None:
+            self._streams = (torch.cuda.current_stream(), torch.cuda.Stream())
+            self._bufs = [torch.empty(q1 - q0, dtype=y_local.dtype, device=y_local.device)
+                          for _, q0, q1 in p.recvs]
+            self._ev_halo = torch.cuda.Event()
+            self._ev_recv = torch.cuda.Event()
+        comp, comm = self._streams
+        if not overlap or (not p.sends and not p.recvs):
+            self.ex.apply_device(x_local, y_local, comp)
+            comm.wait_stream(comp)
+            with torch.cuda.stream(comm):
+                works = self._post(y_local, self._bufs)
+                for w in works:
+                    w.wait()
+                self._ev_recv.record(comm)
+        else:
+            self.ex.apply_device_part(x_local, y_local, 0, comp)  # zero y + boundary rows
+            self._ev_halo.record(comp)
+            comm.wait_event(self._ev_halo)
+            with torch.cuda.stream(comm):
+                works = self._post(y_local, self._bufs)
+                for w in works:
+                    w.wait()
+                self._ev_recv.record(comm)
+            self.ex.apply_device_part(x_local, y_local, 1, comp)  # interior, overlaps the halo
+        comp.wait_event(self._ev_recv)
+        for (peer, q0, q1), buf in zip(p.recvs, self._bufs):
+            self.ex.halo_accumulate(y_local, q0 - p.lo, buf, q1 - q0, comp)
+        return y_local
+
+
+def gather_product(plan: HaloPlan, y_local, world_y: Optional[np.ndarray] = None):
+    """Owned rows of y_local as numpy (rows [row_begin, row_end))."""
+    arr = y_local.detach().cpu().numpy() if hasattr(y_local, "detach") else np.asarray(y_local)
+    own = arr[plan.row_begin - plan.lo:]
+    if world_y is not None:
+        world_y[plan.row_begin:plan.row_end] = own
+    return own

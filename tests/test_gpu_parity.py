@@ -1,0 +1,286 @@
+"""GPU parity: every sm_100a kernel against the reference's own outputs
+(golden vectors made by running the reference, tests/golden/) and against the
+oracle. Tolerances (BASELINE.json north star): fp64 relative L2 <= 1e-12 (we
+also require the reference's inf-norm 1e-12, bench.hpp:93-100); fp32 relative
+L2 <= 1e-5 against the fp64 oracle on fp32-rounded inputs."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle
+
+import paper_1003_0952_b200 as P
+
+from .helpers import family, known_answers, matrix_from_dict, meshes, rel_inf, rel_l2, round32
+
+pytestmark = pytest.mark.gpu
+
+O = Oracle()
+KA = known_answers()
+FAM = family()
+MESH = meshes()
+K = P.StrategyKind
+A = P.AccumMethod
+
+STRATEGIES = [
+    ("sequential", P.Strategy(K.sequential)),
+    ("windowed", P.Strategy(K.windowed)),
+    ("atomic", P.Strategy(K.atomic)),
+    ("colorful_nbh", P.Strategy(K.colorful, p=4)),
+    ("colorful_exact", P.Strategy(K.colorful, p=4, conflict_mode=P.ConflictMode.exact)),
+    ("lb_all_in_one", P.Strategy(K.local_buffers, A.all_in_one, p=4)),
+    ("lb_per_buffer", P.Strategy(K.local_buffers, A.per_buffer, p=4)),
+    ("lb_effective", P.Strategy(K.local_buffers, A.effective, p=4)),
+    ("lb_interval", P.Strategy(K.local_buffers, A.interval, p=4)),
+]
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+def run(a, x, s, transpose=False):
+    ex = P.GpuSpmv(a, s)
+    try:
+        return ex.apply(x, transpose=transpose)
+    finally:
+        ex.close()
+
+
+@pytest.mark.parametrize("name,s", STRATEGIES, ids=[n for n, _ in STRATEGIES])
+def test_known_answers(name, s):
+    for key in ("spmv_diag", "spmv_2x2"):
+        ka = KA[key]
+        a = matrix_from_dict(ka["matrix"])
+        assert run(a, ka["x"], s).tolist() == ka["y"]
+
+
+@pytest.mark.parametrize("name,s", STRATEGIES, ids=[n for n, _ in STRATEGIES])
+@pytest.mark.parametrize("idx", range(29))
+def test_family(name, s, idx):
+    p = f"m{idx}_"
+    a = FAM.matrix(p)
+    for xk, yk in (("x", "y"), ("xr", "yr")):
+        y = run(a, FAM[p + xk], s)
+        assert rel_l2(y, FAM[p + yk]) <= TOL64
+        assert rel_inf(y, FAM[p + yk]) <= TOL64
+
+
+@pytest.mark.parametrize("idx", range(29))
+def test_family_transpose(idx):
+    p = f"m{idx}_"
+    a = FAM.matrix(p)
+    y = P.spmv_csrc_transpose(a, FAM[p + "xr"])
+    assert rel_l2(y, FAM[p + "yt"]) <= TOL64
+
+
+@pytest.mark.parametrize("name,s", STRATEGIES, ids=[n for n, _ in STRATEGIES])
+@pytest.mark.parametrize("idx", range(6))
+def test_meshes(name, s, idx):
+    p = f"g{idx}_"
+    a = MESH.matrix(p)
+    y = run(a, MESH[p + "x"], s)
+    assert rel_l2(y, MESH[p + "y"]) <= TOL64
+
+
+@pytest.mark.parametrize("kind", [K.windowed, K.atomic, K.colorful])
+@pytest.mark.parametrize("idx", range(6))
+def test_meshes_fp32(kind, idx):
+    p = f"g{idx}_"
+    a = MESH.matrix(p)
+    x32 = MESH[p + "x"].astype(np.float32).astype(np.float64)
+    ref = O.spmv_csrc(round32(a), x32)
+    y = run(a, x32, P.Strategy(kind, p=4, dtype=P.DType.f32))
+    assert rel_l2(y, ref) <= TOL32
+
+
+def test_p1_matches_the_reference_path():
+    """p = 1 short-circuits (parallel.hpp:197-202): no buffers, same result."""
+    a = MESH.matrix("g1_")
+    ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, A.effective, p=1))
+    assert ex.buffers_allocated() == 0
+    assert rel_l2(ex.apply(MESH["g1_x"]), MESH["g1_y"]) <= TOL64
+    ex.close()
+    ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, A.effective, p=4))
+    assert ex.buffers_allocated() > 0
+    ex.close()
+
+
+def test_explicit_local_buffers_plan_2x2():
+    """test_parallel.cpp:59-79: p=2, blocks {0},{1} -> (14, 5)."""
+    ka = KA["spmv_2x2"]
+    a = matrix_from_dict(ka["matrix"])
+    part = P.RowPartition(2, [0, 1, 2], [1, 2])
+    ranges = P.effective_ranges(a, part)
+    plan = P.LocalBuffersPlan(part, ranges, P.build_interval_plan(ranges))
+    for acc in A:
+        ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, acc, p=2), plan)
+        assert ex.apply(ka["x"]).tolist() == [14.0, 5.0]
+        assert ex.buffers_allocated() == 2
+        ex.close()
+
+
+def test_mismatched_plans_throw():
+    """test_parallel.cpp:159-165."""
+    a = MESH.matrix("g0_")
+    lb = P.LocalBuffersPlan.build(a, 3)
+    with pytest.raises(P.Error, match="plan built for p=3, strategy has p=4"):
+        P.GpuSpmv(a, P.Strategy(K.local_buffers, p=4), lb)
+    with pytest.raises(P.Error, match="local-buffers plan given to a different strategy"):
+        P.GpuSpmv(a, P.Strategy(K.colorful, p=3), lb)
+    cp = P.ColorfulPlan.build(a, 3)
+    with pytest.raises(P.Error, match="colorful plan given to a different strategy"):
+        P.GpuSpmv(a, P.Strategy(K.local_buffers, p=3), cp)
+
+
+@pytest.mark.parametrize("idx", range(29))
+def test_explicit_colorings_all_orders(idx):
+    p = f"m{idx}_"
+    if not FAM.has(p + "col00"):
+        pytest.skip("no colouring stored")
+    a = FAM.matrix(p)
+    for mode in (0, 1):
+        for order in (0, 1, 2):
+            plan = P.ColorfulPlan(P.Coloring(FAM[p + f"col{mode}{order}"], int(FAM[p + f"nc{mode}{order}"])))
+            ex = P.GpuSpmv(a, P.Strategy(K.colorful, p=4), plan)
+            assert ex.info().n_colors == plan.coloring.n_colors
+            assert rel_l2(ex.apply(FAM[p + "x"]), FAM[p + "y"]) <= TOL64
+            ex.close()
+
+
+def test_corrupt_coloring_is_rejected():
+    """bench_main.cpp:238-249 --corrupt-coloring: merged classes are detected."""
+    a = MESH.matrix("g1_")
+    c = P.color_rows(a)
+    bad = c.color.copy()
+    bad[bad == 1] = 0
+    with pytest.raises(P.Error, match="coloring violation"):
+        P.GpuSpmv(a, P.Strategy(K.colorful, p=2), P.ColorfulPlan(P.Coloring(bad, c.n_colors)))
+
+
+def test_colorful_repeats_are_bit_identical():
+    """test_parallel.cpp:115-123 (atomic-free variant)."""
+    a = MESH.matrix("g5_")
+    ex = P.GpuSpmv(a, P.Strategy(K.colorful, p=4))
+    y1 = ex.apply(MESH["g5_x"])
+    for _ in range(5):
+        assert np.array_equal(ex.apply(MESH["g5_x"]), y1)
+    ex.close()
+
+
+def test_x_length_error():
+    a = MESH.matrix("g0_")
+    ex = P.GpuSpmv(a, P.Strategy(K.windowed))
+    with pytest.raises(P.Error, match=f"x has length 3, expected {a.n}"):
+        ex.apply(np.ones(3))
+    ex.close()
+    with pytest.raises(P.Error, match=f"spmv_csrc: x has length 3, expected {a.n}"):
+        P.spmv_csrc(a, np.ones(3))
+
+
+def test_timings_populated():
+    """test_parallel.cpp:167-177."""
+    a, x, _ = P.config_matrix("c2")
+    for s in (P.Strategy(K.windowed), P.Strategy(K.local_buffers, A.interval, p=4)):
+        ex = P.GpuSpmv(a, s)
+        ex.set_timing(True)
+        ex.apply(x)
+        t = ex.last_timings()
+        assert t.compute_max > 0 and t.init_max >= 0 and t.accumulate_max >= 0
+        ex.close()
+
+
+def test_edge_cases():
+    # n = 0
+    e = P.CsrcMatrix(0, [], [0], [], [], [])
+    assert P.spmv_csrc(e, []).size == 0
+    # n = 1, no pairs
+    one = P.CsrcMatrix(1, [3.0], [0, 0], [], [], [])
+    assert P.spmv_csrc(one, [2.0]).tolist() == [6.0]
+    # rows without pairs in the middle, value-symmetric matrix
+    a = P.CsrcMatrix(4, [1, 2, 3, 4], [0, 0, 1, 1, 3], [0, 0, 1], [0.5, 0.25, 0.125], [], True)
+    x = np.array([1.0, -2.0, 3.0, 0.5])
+    for name, s in STRATEGIES:
+        assert rel_l2(run(a, x, s), O.spmv_csrc(a, x)) <= TOL64, name
+
+
+def test_device_and_graph_entry_points():
+    import torch
+    a, x, _ = P.config_matrix("c1")
+    ref = O.spmv_csrc(a, x)
+    for s in (P.Strategy(K.windowed), P.Strategy(K.atomic), P.Strategy(K.colorful, p=2),
+              P.Strategy(K.local_buffers, A.effective, p=2)):
+        ex = P.GpuSpmv(a, s)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.full_like(xd, float("nan"))
+        st = torch.cuda.Stream()
+        ex.apply_device(xd, yd, st)
+        st.synchronize()
+        assert rel_l2(yd.cpu().numpy(), ref) <= TOL64
+        yd.fill_(float("nan"))
+        for _ in range(3):
+            ex.apply_device_graph(xd, yd, st)
+        st.synchronize()
+        assert rel_l2(yd.cpu().numpy(), ref) <= TOL64
+        ex.close()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+@pytest.mark.parametrize("kind", [K.windowed, K.atomic, K.colorful, K.local_buffers])
+def test_configs_full_size(cfg, kind):
+    a, x, _ = P.config_matrix(cfg)
+    ref = O.spmv_csrc(a, x)
+    y = run(a, x, P.Strategy(kind, p=8))
+    assert rel_l2(y, ref) <= TOL64 and rel_inf(y, ref) <= TOL64
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_large_configs_windowed(cfg):
+    a, x, _ = P.config_matrix(cfg)
+    ref = O.spmv_csrc(a, x)
+    y = run(a, x, P.Strategy(K.windowed))
+    assert rel_l2(y, ref) <= TOL64
+    # linearity, a size-independent property: A(x + 2 z) = A x + 2 A z
+    z = np.random.default_rng(1).uniform(-1, 1, a.n)
+    ex = P.GpuSpmv(a, P.Strategy(K.windowed))
+    lhs = ex.apply(x + 2 * z)
+    rhs = ex.apply(x) + 2 * ex.apply(z)
+    assert rel_l2(lhs, rhs) <= 1e-13
+    ex.close()
+
+
+def test_c5_fp32():
+    a, x, _ = P.config_matrix("c5")
+    x32 = x.astype(np.float32).astype(np.float64)
+    ref = O.spmv_csrc(round32(a), x32)
+    y = run(a, x32, P.Strategy(K.windowed, dtype=P.DType.f32))
+    assert rel_l2(y, ref) <= TOL32
+
+
+@pytest.mark.parametrize("bands", [2, 3, 5])
+@pytest.mark.parametrize("mesh", ["g1_", "g3_", "g5_"])
+def test_band_plans_assemble_the_product(bands, mesh):
+    """Multi-GPU decomposition on one device: each band's plan produces its
+    owned rows plus the halo partial owed to lower bands; summing the halos
+    into their owners (the NCCL exchange of paper_1003_0952_b200.dist)
+    reproduces the full product."""
+    import torch
+    a = MESH.matrix(mesh)
+    x = MESH[mesh + "x"]
+    part = P.partition_by_nnz(a, bands)
+    y = np.zeros(a.n)
+    xd_full = torch.from_numpy(x).cuda()
+    for b in range(bands):
+        r0, r1 = part.begin(b), part.end(b)
+        ex = P.GpuSpmv(a, P.Strategy(K.windowed), band=(r0, r1))
+        inf = ex.info()
+        lo = inf.lo
+        xd = xd_full[lo:r1].contiguous()
+        yd = torch.zeros_like(xd)
+        if b % 2 == 0:
+            ex.apply_device(xd, yd)
+        else:  # boundary rows first, then the interior (overlap form)
+            ex.apply_device_part(xd, yd, 0)
+            ex.apply_device_part(xd, yd, 1)
+        torch.cuda.synchronize()
+        y[lo:r1] += yd.cpu().numpy()
+        assert ex.band_split() >= r0
+        ex.close()
+    assert rel_l2(y, MESH[mesh + "y"]) <= TOL64
