@@ -152,19 +152,36 @@ def run_reference_arm(args, world, rank):
                          a.au.astype(np.float32).astype(np.float64))
         x = x.astype(np.float32).astype(np.float64)
     threads = os.cpu_count() or 1
+    from oracle.oracle import Oracle, Ref
     per_step = []
-    res = None
-    for i in range(args.warmup + args.steps):
-        res = cpu_reference(a, x, args.ref_seconds / max(args.steps, 1), threads)
-        if i >= args.warmup:
-            per_step.append(res["seconds"] / res["reps"])
+    if Ref.available():
+        R = Ref()
+        h = R.exec_create(a, 1, 3, threads)  # ParallelSpmv local_buffers/interval, p = host threads
+        dt1, _, _ = R.exec_run(h, x, 1, a.n)
+        reps = max(1, int(args.ref_seconds / args.steps / max(dt1, 1e-6)))
+        for i in range(args.warmup + args.steps):
+            dt, _, _ = R.exec_run(h, x, reps if i >= args.warmup else 1, a.n)
+            if i >= args.warmup:
+                per_step.append(dt / reps)
+        R.exec_destroy(h)
+        res = dict(kind="reference", cores=threads,
+                   sample=f"each step = {reps} products of the full workload through the reference "
+                          f"ParallelSpmv (local_buffers/interval, p={threads}, oracle/_ref)")
+    else:
+        O = Oracle()
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            O.spmv_csrc(a, x)
+            if i >= args.warmup:
+                per_step.append(time.perf_counter() - t0)
+        res = dict(kind="port", cores=1, sample="each step = 1 product, plain-C oracle port (1 thread)")
     ms = 1e3 * statistics.median(per_step)
     flops = 2 * a.nnz_full()
     value = flops / (ms / 1e3) / 1e9
     mb = P.model_bytes(a, P.DType.f32 if args.dtype == "f32" else P.DType.f64)
     line = dict(
         metric=METRIC, value=value, unit="GFLOP/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-        ms_per_step=ms, higher_is_better=True, scaling="weak" if world > 1 else "strong",
+        ms_per_step=ms, higher_is_better=True, scaling="strong",
         vs_baseline=None, dtype=args.dtype, data="synthetic",
         config=workload_config(args, a, world), impl="reference",
         effective_gbs=mb / (ms / 1e3) / 1e9,

@@ -1,0 +1,66 @@
+// Drop-in check: the reference's own types and calls (csrc::CsrcMatrix,
+// csrc::Strategy, ParallelSpmv, ColorfulPlan, LocalBuffersPlan) run unchanged
+// through include/csrc_gpu.hpp on the B200 and agree with the reference CPU
+// results. Built by oracle/Makefile against /root/reference headers into
+// oracle/_ref/dropin_test; run by tests/test_dropin_cpp.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+
+#include "csrc/csrc.hpp"
+#define CSRC_GPU_ERROR_TYPE csrc::Error
+#include "csrc_gpu.hpp"
+
+using namespace csrc;
+
+static double max_rel(const Vector& y, const Vector& r) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < r.size(); ++i) {
+        num = std::max(num, std::abs(y[i] - r[i]));
+        den = std::max(den, std::abs(r[i]));
+    }
+    return den == 0 ? num : num / den;
+}
+
+int main() {
+    int fails = 0;
+    double worst = 0;
+    for (int i = 0; i < 12; ++i) {
+        index_t n = 40 + 23 * i;
+        CsrcMatrix c = csr_to_csrc(build_csr(generate_random_sym(n, 0.05 + 0.02 * (i % 4), 4242 + i, i % 3 == 0)));
+        Vector x = bench_source_vector(n);
+        Vector ref = spmv_csrc(c, x);
+        worst = std::max(worst, max_rel(gpu::spmv_csrc(c, x), ref));
+        worst = std::max(worst, max_rel(gpu::spmv_csrc_transpose(c, x), spmv_csrc_transpose(c, x)));
+        for (AccumMethod acc : {AccumMethod::all_in_one, AccumMethod::per_buffer, AccumMethod::effective,
+                                AccumMethod::interval}) {
+            Strategy s{StrategyKind::local_buffers, acc, 3};
+            gpu::ParallelSpmv ex(c, s);  // reference Strategy accepted unchanged
+            worst = std::max(worst, max_rel(ex.apply(x), ref));
+            if (ex.buffers_allocated() < 1) ++fails;
+            gpu::ParallelSpmv ex2(c, s, LocalBuffersPlan::build(c, 3));
+            worst = std::max(worst, max_rel(ex2.apply(x), ref));
+        }
+        ColorfulPlan cp = ColorfulPlan::build(c, 2);
+        gpu::ParallelSpmv exc(c, Strategy{StrategyKind::colorful, AccumMethod::effective, 2}, cp);
+        worst = std::max(worst, max_rel(exc.apply(x), ref));
+        auto [y, t] = gpu::spmv_parallel(c, x, Strategy{StrategyKind::colorful, AccumMethod::effective, 2});
+        worst = std::max(worst, max_rel(y, ref));
+    }
+    // error behaviour: the reference's csrc::Error with its wording
+    try {
+        CsrcMatrix c = csr_to_csrc(build_csr(generate_band(10, 1)));
+        gpu::spmv_csrc(c, Vector(3));
+        ++fails;
+    } catch (const csrc::Error& e) {
+        if (std::string(e.what()).find("x has length 3, expected 10") == std::string::npos) ++fails;
+    }
+    try {
+        CsrcMatrix c = csr_to_csrc(build_csr(generate_band(10, 1)));
+        gpu::ParallelSpmv ex(c, Strategy{StrategyKind::sequential, AccumMethod::effective, 2});
+        ++fails;
+    } catch (const csrc::Error& e) {
+        if (std::string(e.what()).find("sequential strategy requires p = 1") == std::string::npos) ++fails;
+    }
+    std::printf("dropin: max rel err %.3e, failures %d\n", worst, fails);
+    return (worst <= 1e-12 && fails == 0) ? 0 : 1;
+}
