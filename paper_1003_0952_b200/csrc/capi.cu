@@ -179,7 +179,6 @@ void choose_windows(Plan& P, const MatView& a) {
             near_cnt += hist[d];
         }
     P.near_depth = dn;
-    P.ring_near = pow2_at_least(dn + 2 * T);
     P.far_lo = 1;
     P.far_hi = 0;
     P.ring_far = 0;
@@ -201,7 +200,6 @@ void choose_windows(Plan& P, const MatView& a) {
             while (f1 > f0 && hist[f1] == 0) --f1;
             P.far_lo = static_cast<int>(f0);
             P.far_hi = static_cast<int>(f1);
-            P.ring_far = pow2_at_least(f1 - f0 + 1 + 2 * T);
             far_cnt = best;
         }
     }
@@ -243,9 +241,11 @@ void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_
                    DevBuf& d_desc, DevBuf& d_cta_ptr) {
     const int n_tiles = static_cast<int>(tiles.size()) - 1;
     std::vector<std::vector<std::pair<int32_t, int32_t>>> per(static_cast<size_t>(std::max(ctas, 1)));
+    std::vector<int> runs_of(per.size(), 0);
     auto add_run = [&](int cta, int t0, int t1) {
+        const int32_t bank = (runs_of[cta]++ & 1) ? dev::kBank : 0;  // alternate per CTA run
         for (int t = t0; t < t1; ++t) {
-            int32_t flags = (t == t0 ? dev::kRunStart : 0) | (t + 1 == t1 ? dev::kRunEnd : 0);
+            int32_t flags = (t == t0 ? dev::kRunStart : 0) | (t + 1 == t1 ? dev::kRunEnd : 0) | bank;
             per[cta].push_back({t, flags});
         }
     };
@@ -278,15 +278,21 @@ void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_
 
 template <class T>
 dev::StageLayout<T> stage_layout(const Plan& P) {
-    const int xn = P.near_depth + dev::kTileRows;
-    const int xf = P.far_lo <= P.far_hi ? (P.far_hi - P.far_lo) + dev::kTileRows : 0;
-    return dev::StageLayout<T>(P.max_tile_pairs, xn, xf);
+    return dev::StageLayout<T>(P.max_tile_pairs, 0, 0);
+}
+
+// rings hold the window plus every tile that can be live: the one awaiting
+// its lagged flush and up to `stages` in flight (windowed.cuh)
+void size_rings(Plan& P, int stages) {
+    const int live = (stages + 1) * dev::kTileRows;
+    P.ring_near = pow2_at_least(P.near_depth + live);
+    P.ring_far = P.far_lo <= P.far_hi ? pow2_at_least(P.far_hi - P.far_lo + 1 + live) : 0;
 }
 
 template <class T>
 size_t windowed_smem(const Plan& P, int stages) {
     size_t s = static_cast<size_t>(stages) * stage_layout<T>(P).bytes;
-    s += sizeof(T) * (P.ring_near + P.ring_far);
+    s += 2 * sizeof(T) * (P.ring_near + P.ring_far);  // two banks
     return (s + 127) & ~size_t(127);
 }
 
@@ -295,8 +301,7 @@ auto windowed_fn(int L) {
     switch (L) {
         case 1: return dev::k_windowed<T, 1>;
         case 2: return dev::k_windowed<T, 2>;
-        case 4: return dev::k_windowed<T, 4>;
-        default: return dev::k_windowed<T, 8>;
+        default: return dev::k_windowed<T, 4>;
     }
 }
 
@@ -306,7 +311,7 @@ int windowed_blocks_per_sm(const Plan& P, size_t smem) {
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     int nb = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, dev::kTileRows * P.win_lanes,
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 + dev::kTileRows * P.win_lanes,
                                                          smem));
     return nb;
 }
@@ -325,8 +330,7 @@ int pick_win_lanes(count_t k, index_t n) {
     const double avg = n ? static_cast<double>(k) / n : 0.0;
     if (avg <= 6) return 1;
     if (avg <= 16) return 2;
-    if (avg <= 48) return 4;
-    return 8;
+    return 4;  // CTA = producer warp + 128*L consumer threads <= 1024
 }
 
 int env_int(const char* name, int dflt) {
@@ -338,8 +342,8 @@ template <class T>
 void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
                     int requested_bands, bool banded) {
     P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows));
-    if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4 && P.win_lanes != 8)
-        throw Error("windowed lanes per row must be 1, 2, 4 or 8");
+    if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4)
+        throw Error("windowed lanes per row must be 1, 2 or 4");
     choose_windows(P, a);
     const int rows_per_tile = dev::kTileRows;
     count_t max_row = 0;
@@ -356,6 +360,7 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
     const int min_ctas = env_int("CSRC_GPU_MINCTAS", 2);
     for (int st = max_st; st >= 2; --st) {
         P.stages = st;
+        size_rings(P, st);
         P.win_smem = windowed_smem<T>(P, st);
         if (P.win_smem > 227 * 1024) continue;
         per_sm = windowed_blocks_per_sm<T>(P, P.win_smem);
@@ -365,7 +370,8 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
         throw Error("windowed: row with " + std::to_string(max_row) +
                     " pairs exceeds the shared-memory tile budget");
     const int resident = num_sms(P.device) * per_sm;
-    const int run_len = std::max(1, env_int("CSRC_GPU_RUN_LEN", 4));
+    // run length >= stages: alternating ring banks per run (windowed.cuh)
+    const int run_len = std::max(P.stages, env_int("CSRC_GPU_RUN_LEN", 4));
     std::vector<int32_t> band_first;
     std::vector<index_t> bs;
     if (banded) {
@@ -435,10 +441,6 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.max_tile_pairs = P.max_tile_pairs;
     A.stages = P.stages;
     A.stage_bytes = P.stage_bytes;
-    A.x_lo = P.lo;
-    A.x_hi = P.row_end;
-    A.xn_len = P.near_depth + dev::kTileRows;
-    A.xf_len = P.far_lo <= P.far_hi ? (P.far_hi - P.far_lo) + dev::kTileRows : 0;
     return A;
 }
 
@@ -742,7 +744,7 @@ void launch_windowed(const Plan& P, dev::WinArgs<T> A, int ctas, cudaStream_t st
     // per-plan shared-memory size: the attribute is per function, so set it per launch
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(P.win_smem)));
-    fn<<<ctas, dev::kTileRows * P.win_lanes, P.win_smem, st>>>(A);
+    fn<<<ctas, 32 + dev::kTileRows * P.win_lanes, P.win_smem, st>>>(A);
 }
 
 void rec(const Plan& P, int i, cudaStream_t st) {

@@ -10,7 +10,8 @@
 //    per stage, `stages` deep) into shared memory: ia, ad, ja, al, au of the
 //    tile are each one contiguous bulk copy.
 //  * L lanes per row (blockDim = kTileRows * L) walk the row's pairs from
-//    shared memory, following spmv_csrc (kernels.hpp:32-41):
+//    shared memory (consumer warps; one extra producer warp issues the TMA
+//    copies and flushes the rings), following spmv_csrc (kernels.hpp:32-41):
 //      gather   y_i += al[t] * x[ja[t]]      registers, width-L shuffle
 //      scatter  y_j += au[t] * x_i           distance d = i - j:
 //               d <= Dn            -> near ring
@@ -20,12 +21,18 @@
 //    each lane keeps four independent CAS in flight and walks its row's
 //    slots with stride B within a batch, so the slot pairs that neighbouring
 //    rows share (d and d+1) never meet inside one batch.
-//  * Schedule: CTA b processes sched[cta_ptr[b] .. cta_ptr[b+1]); entries
+//  * Warp specialisation, no __syncthreads in the loop: per stage a "full"
+//    mbarrier (TMA complete_tx) and an "empty" mbarrier (one arrival per
+//    consumer warp). The producer warp waits for tile ti to be consumed,
+//    flushes the ring positions that became final, then refills the stage
+//    with tile ti + stages. Consumers never wait on each other.
+//  * Schedule: CTA b processes tiles[cta_ptr[b] .. cta_ptr[b+1]); tiles
 //    flagged kRunStart begin a run of row-contiguous tiles. Within a run the
 //    rings slide: after tile [g0, g1) the positions below g1 - Dn (near) and
-//    g1 - Fmax (far) are final and are flushed. Rings hold >= window + 2
-//    tiles, so that flush never aliases the next tile's slots and a single
-//    __syncthreads per tile suffices. Runs of a few tiles dealt round-robin
+//    g1 - Fmax (far) are final. Rings hold window + stages*tile rows so the
+//    lagged flush never aliases slots of tiles still in flight; consecutive
+//    runs use alternating ring banks (run length >= stages), so a run's
+//    final flush overlaps the next run. Runs of a few tiles dealt round-robin
 //    make all CTAs sweep the matrix as one wavefront (far targets and their
 //    x stay L2-resident); one run per CTA = contiguous bands (used for the
 //    private band buffers of the local-buffers strategy).
@@ -41,7 +48,8 @@ constexpr int kTileRows = 128;      // rows per tile; CTA = kTileRows * L thread
 constexpr int kMaxStages = 8;
 constexpr int kRunStart = 1 << 30;  // flag bits in TileDesc::r0 (rows < 2^29)
 constexpr int kRunEnd = 1 << 29;
-constexpr int kRowMask = kRunEnd - 1;
+constexpr int kBank = 1 << 28;      // ring bank of the tile's run
+constexpr int kRowMask = kBank - 1;
 
 // One tile of a CTA's schedule: rows [r0, r1) (local), pairs [p0, p1);
 // r0 carries kRunStart / kRunEnd.
@@ -71,8 +79,6 @@ struct WinArgs {
     int32_t max_tile_pairs;
     int32_t stages;             // TMA pipeline depth
     int32_t stage_bytes;
-    int32_t x_lo, x_hi;         // global positions valid in x
-    int32_t xn_len, xf_len;     // staged x window capacities (elements)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -135,7 +141,7 @@ __device__ __forceinline__ Seg<E> seg(const E* a, int64_t i0, int64_t i1) {
 //   ia[kTileRows+1] | ad[kTileRows] | ja[P] | al[P] | au[P]
 template <typename T>
 struct StageLayout {
-    int o_ia, o_ad, o_ja, o_al, o_au, o_xn, o_xf, bytes;
+    int o_ia, o_ad, o_ja, o_al, o_au, o_xn, o_xf, bytes;  // o_xn/o_xf: optional x windows
     __host__ __device__ static int al16(int v) { return (v + 15) & ~15; }
     __host__ __device__ static int seg_bytes(int m, int e) { return al16(e * (m + 2 * (16 / e))); }
     // xn_len / xf_len: elements of the near / far x windows (0 = not staged)
@@ -151,27 +157,6 @@ struct StageLayout {
         bytes = o_xf + al16(e * xf_len);
     }
 };
-
-// Inward 16-byte alignment of the x window [q0, q1) (global positions, x
-// indexed as xb[q]): the TMA copy never reads outside [q0, q1); the staged
-// positions are [*w0, *w0 + *wn). Positions outside fall back to LDG.
-template <typename T>
-__device__ __forceinline__ uint32_t x_window(const T* xb, int32_t q0, int32_t q1, int32_t* w0,
-                                             int32_t* wn, const char** src) {
-    *w0 = q0;
-    *wn = 0;
-    *src = nullptr;
-    if (q1 <= q0) return 0;
-    const uintptr_t a = reinterpret_cast<uintptr_t>(xb + q0);
-    const uintptr_t b = reinterpret_cast<uintptr_t>(xb + q1);
-    const uintptr_t a2 = (a + 15) & ~uintptr_t(15);
-    const uintptr_t b2 = b & ~uintptr_t(15);
-    if (b2 <= a2) return 0;
-    *w0 = q0 + static_cast<int32_t>((a2 - a) / sizeof(T));
-    *wn = static_cast<int32_t>((b2 - a2) / sizeof(T));
-    *src = reinterpret_cast<const char*>(a2);
-    return static_cast<uint32_t>(b2 - a2);
-}
 
 // 32-bit shared-memory address forms (no generic-pointer conversions).
 __device__ __forceinline__ double lds_f(uint32_t a, double) {
@@ -201,6 +186,12 @@ __device__ __forceinline__ float cas_s(uint32_t a, float cmp, float val) {
     return __uint_as_float(r);
 }
 
+__device__ __forceinline__ int32_t lds_i(uint32_t a) {
+    int32_t v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
 // Shared-memory CAS of a T, as raw bits.
 __device__ __forceinline__ double cas_bits(double* p, double cmp, double val) {
     return __longlong_as_double(static_cast<long long>(
@@ -219,20 +210,54 @@ __device__ __forceinline__ bool same_bits(float a, float b) {
     return __float_as_int(a) == __float_as_int(b);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kDoneSlots = kMaxStages + 2;  // per-tile "done" barriers (ring)
+
+// Final positions of tile d (stateless: tiles of a run are row-contiguous):
+// near [g0 - Dn, g1 - Dn) and far [g0 - Fmax, g1 - Fmax) while the run goes
+// on; at the run's end everything the run can still hold.
+template <typename T>
+__device__ __forceinline__ void flush_tile(const WinArgs<T>& A, T* __restrict__ out, T* rings,
+                                           int bank_elems, const TileDesc& d, int lane) {
+    const bool far_on = A.far_lo <= A.far_hi;
+    const int32_t g0 = A.row_begin + (d.r0 & kRowMask);
+    const int32_t g1 = A.row_begin + d.r1;
+    T* ringN = rings + ((d.r0 & kBank) ? bank_elems : 0);
+    T* ringF = ringN + A.ring_near;
+    const bool end = (d.r0 & kRunEnd) != 0;
+    auto flush = [&](T* ring, int mask, int32_t from, int32_t to) {
+        if (from < 0) from = 0;
+        for (int32_t q = from + lane; q < to; q += 32) {
+            T* slot = ring + (q & mask);
+            const T v = *slot;
+            if (v != T(0)) {
+                red_add(out + q, v);
+                *slot = T(0);
+            }
+        }
+    };
+    flush(ringN, A.ring_near - 1, g0 - A.near_depth, end ? g1 : g1 - A.near_depth);
+    if (far_on) flush(ringF, A.ring_far - 1, g0 - A.far_hi, end ? g1 - A.far_lo : g1 - A.far_hi);
+}
+
 template <typename T, int L>
-__global__ void __launch_bounds__(kTileRows * L) k_windowed(WinArgs<T> A) {
+__global__ void __launch_bounds__(32 + kTileRows * L) k_windowed(WinArgs<T> A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const StageLayout<T> lay(A.max_tile_pairs, A.xn_len, A.xf_len);
-    __shared__ __align__(8) uint64_t bars[kMaxStages];
+    const StageLayout<T> lay(A.max_tile_pairs, 0, 0);
+    __shared__ __align__(8) uint64_t full[kMaxStages];
+    __shared__ __align__(8) uint64_t empty[kMaxStages];
+    __shared__ __align__(8) uint64_t done[kDoneSlots];
     __shared__ uint32_t offs[kMaxStages][5];
     __shared__ TileDesc descs[kMaxStages];
-    __shared__ int4 xwin[kMaxStages];  // staged x windows: near start, len, far start, len
+    __shared__ TileDesc dring[kDoneSlots];  // descriptors of recent tiles, for the flush
 
-    T* ringN = reinterpret_cast<T*>(smem_raw + A.stages * A.stage_bytes);
-    T* ringF = ringN + A.ring_near;
-
-    constexpr int nthreads = kTileRows * L;
+    constexpr int kConsumerWarps = kTileRows * L / 32;
     const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
     const int maskN = A.ring_near - 1;
     const int maskF = A.ring_far - 1;
     const bool far_on = A.far_lo <= A.far_hi;
@@ -243,193 +268,200 @@ __global__ void __launch_bounds__(kTileRows * L) k_windowed(WinArgs<T> A) {
     const int32_t s0 = A.cta_ptr[b];
     const int32_t t_count = A.cta_ptr[b + 1] - s0;
     if (t_count <= 0) return;
+    const int S = A.stages;
+    const int bank_elems = A.ring_near + A.ring_far;
+    T* rings = reinterpret_cast<T*>(smem_raw + S * A.stage_bytes);
 
-    for (int i = tid; i < A.ring_near + (far_on ? A.ring_far : 0); i += nthreads) ringN[i] = T(0);
+    for (int i = tid; i < 2 * bank_elems; i += blockDim.x) rings[i] = T(0);
     if (tid == 0) {
-        for (int s = 0; s < A.stages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        for (int s = 0; s < kDoneSlots; ++s) mbar_init(&done[s], kConsumerWarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-
-    // thread 0 issues tile ti's TMA copies from its descriptor (no dependent
-    // global loads on the refill path; the next descriptor is prefetched)
-    auto issue = [&](int ti, const TileDesc& d) {
-        const int s = ti % A.stages;
-        const int32_t r0 = d.r0 & kRowMask, r1 = d.r1;
-        unsigned char* st = smem_raw + s * A.stage_bytes;
-        const Seg<int32_t> s_ia = seg(A.ia, r0, r1 + 1);
-        const Seg<T> s_ad = seg(A.ad, r0, r1);
-        const Seg<int32_t> s_ja = seg(A.ja, d.p0, d.p1);
-        const Seg<T> s_al = seg(A.al, d.p0, d.p1);
-        const Seg<T> s_au = seg(A.au, d.p0, d.p1);
-        const uint32_t tx =
-            s_ia.bytes + s_ad.bytes + s_ja.bytes + s_al.bytes + (sym ? 0u : s_au.bytes);
-        offs[s][0] = s_ia.off;
-        offs[s][1] = s_ad.off;
-        offs[s][2] = s_ja.off;
-        offs[s][3] = s_al.off;
-        offs[s][4] = s_au.off;
-        descs[s] = d;
-        // x windows of the tile's ring targets (and own rows)
-        const int32_t g0 = A.row_begin + r0, g1 = A.row_begin + r1;
-        const T* xb0 = A.x + A.xshift;
-        int32_t n0, nn, f0, fn;
-        const char *nsrc, *fsrc;
-        uint32_t nb = x_window(xb0, max(g0 - A.near_depth, A.x_lo), min(g1, A.x_hi), &n0, &nn, &nsrc);
-        uint32_t fb = 0;
-        f0 = 0;
-        fn = 0;
-        fsrc = nullptr;
-        if (A.xf_len > 0)
-            fb = x_window(xb0, max(g0 - A.far_hi, A.x_lo), min(g1 - A.far_lo, A.x_hi), &f0, &fn, &fsrc);
-        xwin[s] = make_int4(n0, nn, f0, fn);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[s], tx + nb + fb);
-        if (nb) tma_load(st + lay.o_xn, nsrc, nb, &bars[s]);
-        if (fb) tma_load(st + lay.o_xf, fsrc, fb, &bars[s]);
-        tma_load(st + lay.o_ia, s_ia.src, s_ia.bytes, &bars[s]);
-        tma_load(st + lay.o_ad, s_ad.src, s_ad.bytes, &bars[s]);
-        tma_load(st + lay.o_ja, s_ja.src, s_ja.bytes, &bars[s]);
-        tma_load(st + lay.o_al, s_al.src, s_al.bytes, &bars[s]);
-        if (!sym) tma_load(st + lay.o_au, s_au.src, s_au.bytes, &bars[s]);
-    };
     const TileDesc* my = A.tiles + s0;
-    TileDesc next{};  // thread 0: descriptor of the next tile to issue
-    if (tid == 0) {
-        for (int ti = 0; ti < A.stages && ti < t_count; ++ti) issue(ti, my[ti]);
-        if (A.stages < t_count) next = my[A.stages];
+
+    if (warp == 0) {
+        // ------------------------------------------------------- producer
+        if (lane != 0) return;
+        auto issue = [&](int ti, const TileDesc& d) {
+            const int s = ti % S;
+            const int32_t r0 = d.r0 & kRowMask, r1 = d.r1;
+            unsigned char* st = smem_raw + s * A.stage_bytes;
+            const Seg<int32_t> s_ia = seg(A.ia, r0, r1 + 1);
+            const Seg<T> s_ad = seg(A.ad, r0, r1);
+            const Seg<int32_t> s_ja = seg(A.ja, d.p0, d.p1);
+            const Seg<T> s_al = seg(A.al, d.p0, d.p1);
+            const Seg<T> s_au = seg(A.au, d.p0, d.p1);
+            const uint32_t tx =
+                s_ia.bytes + s_ad.bytes + s_ja.bytes + s_al.bytes + (sym ? 0u : s_au.bytes);
+            offs[s][0] = s_ia.off;
+            offs[s][1] = s_ad.off;
+            offs[s][2] = s_ja.off;
+            offs[s][3] = s_al.off;
+            offs[s][4] = s_au.off;
+            descs[s] = d;
+            dring[ti % kDoneSlots] = d;
+            // no proxy fence: the empty-barrier wait orders the consumers'
+            // reads of this stage before the TMA overwrite (standard pipeline)
+            mbar_expect_tx(&full[s], tx);
+            tma_load(st + lay.o_ia, s_ia.src, s_ia.bytes, &full[s]);
+            tma_load(st + lay.o_ad, s_ad.src, s_ad.bytes, &full[s]);
+            tma_load(st + lay.o_ja, s_ja.src, s_ja.bytes, &full[s]);
+            tma_load(st + lay.o_al, s_al.src, s_al.bytes, &full[s]);
+            if (!sym) tma_load(st + lay.o_au, s_au.src, s_au.bytes, &full[s]);
+        };
+        for (int ti = 0; ti < S && ti < t_count; ++ti) issue(ti, my[ti]);
+        TileDesc next = S < t_count ? my[S] : TileDesc{};
+        for (int ti = S; ti < t_count; ++ti) {
+            const int s = ti % S;
+            mbar_wait(&empty[s], ((ti - S) / S) & 1);  // every consumer is done with tile ti - S
+            issue(ti, next);
+            if (ti + 1 < t_count) next = my[ti + 1];
+        }
+        return;
     }
 
-    auto flush = [&](T* ring, int mask, int32_t from, int32_t to) {
-        if (from < 0) from = 0;
-        for (int32_t q = from + tid; q < to; q += nthreads) {
-            T* slot = ring + (q & mask);
-            const T v = *slot;
-            if (v != T(0)) {
-                red_add(out + q, v);
-                *slot = T(0);
-            }
-        }
-    };
-
-    const int row = tid / L;
-    const int sub = tid % L;
-    int32_t near_done = 0, far_done = 0;  // flushed-below marks of the current run
+    // --------------------------------------------------------------- consumers
+    const int cw = warp - 1;  // consumer warp id
+    const int ctid = tid - 32;
+    const int row = ctid / L;
+    const int sub = ctid % L;
     const int32_t near_depth = A.near_depth, far_lo = A.far_lo;
-    // far ring test as one unsigned compare; an empty far window never matches
     const uint32_t far_span = far_on ? static_cast<uint32_t>(A.far_hi - A.far_lo) : 0u;
-    const uint32_t ringN_s = smem_u32(ringN);
-    const uint32_t ringF_s = far_on ? smem_u32(ringF) : 0u;
     const T* __restrict__ xb = A.x + A.xshift;  // x indexed by global position
-
     for (int ti = 0; ti < t_count; ++ti) {
-        const int s = ti % A.stages;
-        mbar_wait(&bars[s], (ti / A.stages) & 1);
-        const TileDesc dsc = descs[s];
-        const int32_t r0 = dsc.r0 & kRowMask, r1 = dsc.r1;
-        const int nr = r1 - r0;
-        const int32_t g0 = A.row_begin + r0;
-        const int32_t g1 = g0 + nr;
-        if (dsc.r0 & kRunStart) {
-            near_done = g0 - A.near_depth;
-            far_done = g0 - A.far_hi;
+        const int s = ti % S;
+        // lagged flush: tile ti-1 is flushed by consumer warp (ti-1) % W once
+        // every consumer warp has finished it
+        if (ti >= 1 && (ti - 1) % kConsumerWarps == cw) {
+            mbar_wait(&done[(ti - 1) % kDoneSlots], ((ti - 1) / kDoneSlots) & 1);
+            flush_tile(A, out, rings, bank_elems, dring[(ti - 1) % kDoneSlots], lane);
+            __syncwarp();
         }
-        const unsigned char* st = smem_raw + s * A.stage_bytes;
-        const int32_t* ia_s = reinterpret_cast<const int32_t*>(st + lay.o_ia) + offs[s][0];
-        const T* ad_s = reinterpret_cast<const T*>(st + lay.o_ad) + offs[s][1];
-        const int32_t* ja_s = reinterpret_cast<const int32_t*>(st + lay.o_ja) + offs[s][2];
-        const T* al_s = reinterpret_cast<const T*>(st + lay.o_al) + offs[s][3];
-        const T* au_s = sym ? al_s : reinterpret_cast<const T*>(st + lay.o_au) + offs[s][4];
-        const int32_t p0 = ia_s[0];
-        const int4 xw = xwin[s];
-        const T* xn_s = reinterpret_cast<const T*>(st + lay.o_xn);
-        const T* xf_s = reinterpret_cast<const T*>(st + lay.o_xf);
-        auto xget = [&](int32_t q) -> T {  // staged x, else L1/L2
-            if (static_cast<uint32_t>(q - xw.x) < static_cast<uint32_t>(xw.y)) return xn_s[q - xw.x];
-            if (static_cast<uint32_t>(q - xw.z) < static_cast<uint32_t>(xw.w)) return xf_s[q - xw.z];
-            return __ldg(xb + q);
-        };
+        mbar_wait(&full[s], (ti / S) & 1);
+        const TileDesc dsc = descs[s];
+        const int32_t r0 = dsc.r0 & kRowMask;
+        const int nr = dsc.r1 - r0;
+        const int32_t g0 = A.row_begin + r0;
+        const uint32_t ringN_s = smem_u32(rings + ((dsc.r0 & kBank) ? bank_elems : 0));
+        const uint32_t ringF_s = ringN_s + A.ring_near * sizeof(T);
+        // 32-bit shared addresses of the staged segments (no generic pointers)
+        const uint32_t st_s = smem_u32(smem_raw) + s * A.stage_bytes;
+        constexpr uint32_t E = sizeof(T);
+        const uint32_t ia_b = st_s + lay.o_ia + 4u * offs[s][0];
+        const uint32_t ad_b = st_s + lay.o_ad + E * offs[s][1];
+        const uint32_t ja_b0 = st_s + lay.o_ja + 4u * offs[s][2];
+        const uint32_t al_b0 = st_s + lay.o_al + E * offs[s][3];
+        const uint32_t au_b0 = sym ? al_b0 : st_s + lay.o_au + E * offs[s][4];
+        const int32_t p0 = lds_i(ia_b);
 
         const bool act = row < nr;
         const int32_t g = g0 + row;
         T yi = T(0), xi = T(0);
         if (act) {
-            xi = xget(g);
-            const int32_t a0 = ia_s[row] - p0 + sub;
-            const int32_t a1 = ia_s[row + 1] - p0;
-            const int32_t m = a0 < a1 ? (a1 - a0 + L - 1) / L : 0;  // pairs of this lane
-            const int32_t nb = (m + 3) >> 2;                       // batches; stride nb
+            xi = __ldg(xb + g);
+            const int32_t rb = lds_i(ia_b + 4u * row) - p0;
+            const int32_t len = lds_i(ia_b + 4u * (row + 1)) - p0 - rb;
+            // L = 1: the lane's slots in a batch are strided by nb, so the slot
+            // pairs neighbouring rows share (d, d+1) never meet in a batch.
+            // L > 1: sub-lane sub owns the blocked slot range [sub*q, sub*q+m)
+            // (one instruction never pairs d with d+1 across neighbouring rows)
+            const int32_t q = L == 1 ? len : (len + L - 1) / L;
+            const int32_t first = rb + sub * q;
+            const int32_t m = L == 1 ? len : max(0, min(q, len - sub * q));
+            const int32_t nb = (m + 3) >> 2;
+            const uint32_t ja_b = ja_b0 + 4u * first;
+            const uint32_t al_b = al_b0 + E * first;
+            const uint32_t au_b = au_b0 + E * first;
             for (int32_t bt = 0; bt < nb; ++bt) {
-                int32_t t[4], j[4];
-                bool ok[4];
+                int32_t mm[4], j[4];
                 T xv[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int32_t mm = bt + u * nb;
-                    ok[u] = mm < m;
-                    t[u] = a0 + mm * L;
-                    j[u] = ok[u] ? ja_s[t[u]] : g;
+                    mm[u] = L == 1 ? bt + u * nb : 4 * bt + u;
+                    j[u] = mm[u] < m ? lds_i(ja_b + 4u * mm[u]) : -1;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) xv[u] = ok[u] ? xget(j[u]) : T(0);
-                // ring slot (shared address) per pair; 0 = spill / none
+                for (int u = 0; u < 4; ++u) xv[u] = j[u] >= 0 ? __ldg(xb + j[u]) : T(0);
                 uint32_t sa[4];
-                T val[4], old[4];
+                T val[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const T alv = ok[u] ? al_s[t[u]] : T(0);
-                    const T auv = ok[u] ? au_s[t[u]] : T(0);
-                    yi += alv * xv[u];
-                    val[u] = auv * xi;
-                    const int32_t d = g - j[u];
-                    const bool nearw = d <= near_depth;
-                    const bool farw = static_cast<uint32_t>(d - far_lo) <= far_span;
-                    sa[u] = !ok[u] ? 0u
-                            : nearw ? ringN_s + (static_cast<uint32_t>(j[u] & maskN) * sizeof(T))
-                            : farw  ? ringF_s + (static_cast<uint32_t>(j[u] & maskF) * sizeof(T))
-                                    : 0u;
-                    if (ok[u] && !nearw && !farw) red_add(out + j[u], val[u]);
+                    sa[u] = 0u;
+                    val[u] = T(0);
+                    if (j[u] >= 0) {
+                        yi = fma(lds_f(al_b + E * mm[u], T(0)), xv[u], yi);
+                        val[u] = lds_f(au_b + E * mm[u], T(0)) * xi;
+                        const int32_t d = g - j[u];
+                        if (d <= near_depth)
+                            sa[u] = ringN_s + E * static_cast<uint32_t>(j[u] & maskN);
+                        else if (static_cast<uint32_t>(d - far_lo) <= far_span && far_on)
+                            sa[u] = ringF_s + E * static_cast<uint32_t>(j[u] & maskF);
+                        else
+                            red_add(out + j[u], val[u]);
+                    }
                 }
-                // four independent CAS in flight; retry only on a lost race
+                if (L == 1) {
+                    T old[4];  // four independent CAS in flight
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (sa[u]) old[u] = lds_f(sa[u], T(0));
+                    for (int u = 0; u < 4; ++u)
+                        if (sa[u]) old[u] = lds_f(sa[u], T(0));
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (!sa[u]) continue;
-                    T seen = cas_s(sa[u], old[u], old[u] + val[u]);
-                    while (!same_bits(seen, old[u])) {
-                        old[u] = seen;
-                        seen = cas_s(sa[u], old[u], old[u] + val[u]);
+                    for (int u = 0; u < 4; ++u) {
+                        if (!sa[u]) continue;
+                        T seen = cas_s(sa[u], old[u], old[u] + val[u]);
+                        while (!same_bits(seen, old[u])) {
+                            old[u] = seen;
+                            seen = cas_s(sa[u], old[u], old[u] + val[u]);
+                        }
+                    }
+                } else {
+                    // consecutive slots of one lane may pair d with d+1 across
+                    // rows: read each old value right before its CAS
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (!sa[u]) continue;
+                        T o = lds_f(sa[u], T(0));
+                        T seen = cas_s(sa[u], o, o + val[u]);
+                        while (!same_bits(seen, o)) {
+                            o = seen;
+                            seen = cas_s(sa[u], o, o + val[u]);
+                        }
                     }
                 }
             }
         }
-        // all 32 lanes reach the width-L reduction (rows >= nr contribute 0)
+        // all lanes reach the width-L reduction (rows >= nr contribute 0)
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) yi += __shfl_xor_sync(0xffffffffu, yi, off, L);
-        if (act && sub == 0) atomicAdd(ringN + (g & maskN), yi + ad_s[row] * xi);
-
-        __syncthreads();  // stage s consumed; the tile's ring contributions complete
-        if (tid == 0 && ti + A.stages < t_count) {
-            issue(ti + A.stages, next);
-            if (ti + A.stages + 1 < t_count) next = my[ti + A.stages + 1];
-        }
-        const bool run_ends = (dsc.r0 & kRunEnd) != 0;
-        if (run_ends) {
-            flush(ringN, maskN, near_done, g1);
-            if (far_on) flush(ringF, maskF, far_done, g1 - A.far_lo);
-            __syncthreads();  // the next run's window may alias these slots
-        } else {
-            // slide: positions no later row of the run can reach are final;
-            // rings hold window + 2 tiles, so the next tile never aliases them
-            flush(ringN, maskN, near_done, g1 - A.near_depth);
-            near_done = g1 - A.near_depth;
-            if (far_on) {
-                flush(ringF, maskF, far_done, g1 - A.far_hi);
-                far_done = g1 - A.far_hi;
+        if (act && sub == 0) {
+            const uint32_t a = ringN_s + static_cast<uint32_t>(g & maskN) * sizeof(T);
+            const T add = yi + lds_f(ad_b + E * row, T(0)) * xi;
+            T old0 = lds_f(a, T(0));
+            T seen = cas_s(a, old0, old0 + add);
+            while (!same_bits(seen, old0)) {
+                old0 = seen;
+                seen = cas_s(a, old0, old0 + add);
             }
         }
+        // mbarrier arrive has release semantics for this warp's shared-memory
+        // updates (ordered by __syncwarp); no MEMBAR that would also wait for
+        // the flush's outstanding red.global ops
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[s]);                   // stage s may be refilled
+            mbar_arrive(&done[ti % kDoneSlots]);      // tile ti's ring contributions are in
+        }
+    }
+    // the last tile's flush
+    const int tl = t_count - 1;
+    if (tl % kConsumerWarps == cw) {
+        mbar_wait(&done[tl % kDoneSlots], (tl / kDoneSlots) & 1);
+        flush_tile(A, out, rings, bank_elems, dring[tl % kDoneSlots], lane);
     }
 }
 
