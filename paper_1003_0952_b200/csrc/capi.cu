@@ -94,6 +94,7 @@ struct csrc_gpu_plan_s {
     int max_tile_pairs = 16;
     size_t win_smem = 0;
     int win_lanes = 1;     // L lanes per row in the windowed kernel
+    int tile_rows = 128;   // rows per tile (64 or 128)
     int stages = 2;
     int stage_bytes = 0;
     double captured = 0.0;
@@ -161,7 +162,7 @@ void upload_values(DevBuf& d, const double* h, size_t count) {
 // distance window beyond Dn; the rest spills to red.global.add. Rings hold
 // the window plus two tiles (see windowed.cuh).
 void choose_windows(Plan& P, const MatView& a) {
-    const int T = dev::kTileRows;
+    const int T = P.tile_rows;
     const int kRingMax = 2048;
     count_t maxd = 0;
     for (index_t r = P.row_begin; r < P.row_end; ++r)
@@ -220,7 +221,7 @@ std::vector<int32_t> make_tiles(const Plan& P, const MatView& a, const std::vect
         const index_t e = bs[b + 1];
         while (r < e) {
             tiles.push_back(r);
-            const index_t lim = std::min<index_t>(r + dev::kTileRows, e);
+            const index_t lim = std::min<index_t>(r + P.tile_rows, e);
             index_t end = r + 1;  // grow while the pair budget holds
             while (end < lim &&
                    static_cast<count_t>(a.ia[g + end + 1]) - a.ia[g + r] <= P.max_tile_pairs)
@@ -278,13 +279,13 @@ void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_
 
 template <class T>
 dev::StageLayout<T> stage_layout(const Plan& P) {
-    return dev::StageLayout<T>(P.max_tile_pairs, 0, 0);
+    return dev::StageLayout<T>(P.max_tile_pairs, 0, 0, P.tile_rows);
 }
 
 // rings hold the window plus every tile that can be live: the one awaiting
 // its lagged flush and up to `stages` in flight (windowed.cuh)
 void size_rings(Plan& P, int stages) {
-    const int live = (stages + 1) * dev::kTileRows;
+    const int live = (stages + 1) * P.tile_rows;
     P.ring_near = pow2_at_least(P.near_depth + live);
     P.ring_far = P.far_lo <= P.far_hi ? pow2_at_least(P.far_hi - P.far_lo + 1 + live) : 0;
 }
@@ -297,21 +298,35 @@ size_t windowed_smem(const Plan& P, int stages) {
 }
 
 template <class T>
-auto windowed_fn(int L) {
+auto windowed_fn(int L, int TR) {
+    if (TR == 32) {
+        switch (L) {
+            case 1: return dev::k_windowed<T, 1, 32>;
+            case 2: return dev::k_windowed<T, 2, 32>;
+            default: return dev::k_windowed<T, 4, 32>;
+        }
+    }
+    if (TR == 64) {
+        switch (L) {
+            case 1: return dev::k_windowed<T, 1, 64>;
+            case 2: return dev::k_windowed<T, 2, 64>;
+            default: return dev::k_windowed<T, 4, 64>;
+        }
+    }
     switch (L) {
-        case 1: return dev::k_windowed<T, 1>;
-        case 2: return dev::k_windowed<T, 2>;
-        default: return dev::k_windowed<T, 4>;
+        case 1: return dev::k_windowed<T, 1, 128>;
+        case 2: return dev::k_windowed<T, 2, 128>;
+        default: return dev::k_windowed<T, 4, 128>;
     }
 }
 
 template <class T>
 int windowed_blocks_per_sm(const Plan& P, size_t smem) {
-    auto fn = windowed_fn<T>(P.win_lanes);
+    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows);
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     int nb = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 + dev::kTileRows * P.win_lanes,
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 + P.tile_rows * P.win_lanes,
                                                          smem));
     return nb;
 }
@@ -325,7 +340,7 @@ MatView local_view(const MatView& a, index_t r0, index_t r1) {
     return v;
 }
 
-int pick_win_lanes(count_t k, index_t n) {
+int pick_win_lanes(count_t k, index_t n) {  // see profiles/r01_sweep10.txt
     // measured on B200 (profiles/r01_sweep*.txt): ~6 pairs per lane is best
     const double avg = n ? static_cast<double>(k) / n : 0.0;
     if (avg <= 6) return 1;
@@ -344,8 +359,15 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
     P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows));
     if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4)
         throw Error("windowed lanes per row must be 1, 2 or 4");
+    {   // ~1.7K pairs (~35 KB of fp64 matrix data) per tile: big TMA copies
+        const double avg = P.nrows ? static_cast<double>(P.k) / P.nrows : 0.0;
+        (void)avg;  // profiles/r01_sweep13-14: 128-row tiles win on every config
+        P.tile_rows = env_int("CSRC_GPU_TILE", 128);
+    }
+    if (P.tile_rows != 32 && P.tile_rows != 64 && P.tile_rows != 128)
+        throw Error("windowed tile rows must be 32, 64 or 128");
     choose_windows(P, a);
-    const int rows_per_tile = dev::kTileRows;
+    const int rows_per_tile = P.tile_rows;
     count_t max_row = 0;
     for (index_t r = P.row_begin; r < P.row_end; ++r)
         max_row = std::max<count_t>(max_row, a.ia[r + 1] - a.ia[r]);
@@ -740,11 +762,11 @@ template <class T>
 void launch_windowed(const Plan& P, dev::WinArgs<T> A, int ctas, cudaStream_t st) {
     if (ctas <= 0) return;
     if (P.value_symmetric) A.au = A.al;
-    auto fn = windowed_fn<T>(P.win_lanes);
+    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows);
     // per-plan shared-memory size: the attribute is per function, so set it per launch
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(P.win_smem)));
-    fn<<<ctas, 32 + dev::kTileRows * P.win_lanes, P.win_smem, st>>>(A);
+    fn<<<ctas, 32 + P.tile_rows * P.win_lanes, P.win_smem, st>>>(A);
 }
 
 void rec(const Plan& P, int i, cudaStream_t st) {

@@ -44,7 +44,7 @@
 namespace csrcgpu {
 namespace dev {
 
-constexpr int kTileRows = 128;      // rows per tile; CTA = kTileRows * L threads
+constexpr int kTileRows = 128;      // max rows per tile (TR = 32/64/128); CTA = 32 + TR * L threads
 constexpr int kMaxStages = 8;
 constexpr int kRunStart = 1 << 30;  // flag bits in TileDesc::r0 (rows < 2^29)
 constexpr int kRunEnd = 1 << 29;
@@ -145,11 +145,11 @@ struct StageLayout {
     __host__ __device__ static int al16(int v) { return (v + 15) & ~15; }
     __host__ __device__ static int seg_bytes(int m, int e) { return al16(e * (m + 2 * (16 / e))); }
     // xn_len / xf_len: elements of the near / far x windows (0 = not staged)
-    __host__ __device__ StageLayout(int max_pairs, int xn_len, int xf_len) {
+    __host__ __device__ StageLayout(int max_pairs, int xn_len, int xf_len, int tile_rows = kTileRows) {
         const int e = static_cast<int>(sizeof(T));
         o_ia = 0;
-        o_ad = o_ia + seg_bytes(kTileRows + 1, 4);
-        o_ja = o_ad + seg_bytes(kTileRows, e);
+        o_ad = o_ia + seg_bytes(tile_rows + 1, 4);
+        o_ja = o_ad + seg_bytes(tile_rows, e);
         o_al = o_ja + seg_bytes(max_pairs, 4);
         o_au = o_al + seg_bytes(max_pairs, e);
         o_xn = o_au + seg_bytes(max_pairs, e);
@@ -243,10 +243,10 @@ __device__ __forceinline__ void flush_tile(const WinArgs<T>& A, T* __restrict__ 
     if (far_on) flush(ringF, A.ring_far - 1, g0 - A.far_hi, end ? g1 - A.far_lo : g1 - A.far_hi);
 }
 
-template <typename T, int L>
-__global__ void __launch_bounds__(32 + kTileRows * L) k_windowed(WinArgs<T> A) {
+template <typename T, int L, int TR>
+__global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const StageLayout<T> lay(A.max_tile_pairs, 0, 0);
+    const StageLayout<T> lay(A.max_tile_pairs, 0, 0, TR);
     __shared__ __align__(8) uint64_t full[kMaxStages];
     __shared__ __align__(8) uint64_t empty[kMaxStages];
     __shared__ __align__(8) uint64_t done[kDoneSlots];
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(32 + kTileRows * L) k_windowed(WinArgs<T> A) {
     __shared__ TileDesc descs[kMaxStages];
     __shared__ TileDesc dring[kDoneSlots];  // descriptors of recent tiles, for the flush
 
-    constexpr int kConsumerWarps = kTileRows * L / 32;
+    constexpr int kConsumerWarps = TR * L / 32;
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
