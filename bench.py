@@ -210,7 +210,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--kind", default="windowed", choices=["windowed", "atomic", "colorful", "local_buffers"])
+    ap.add_argument("--kind", default="gather", choices=["gather", "windowed", "atomic", "colorful", "local_buffers"])
+    ap.add_argument("--compare", default="windowed,atomic",
+                    help="other kernels timed on the same workload (reported under 'kernels'); '' = none")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -250,7 +252,19 @@ def main():
         ms = float(np.mean(tot))
         kms = float(np.mean(ker))
         info = ex.info()
-        launches_per_step = 1 if args.kind in ("windowed", "atomic") else info.launches_per_apply
+        # our kernels per product (the y memset of windowed/atomic is a driver memset, not counted)
+        launches_per_step = 1 if args.kind in ("gather", "windowed", "atomic") else info.launches_per_apply
+        others = {}
+        for name in [k for k in args.compare.split(",") if k and k != args.kind]:
+            ox = P.GpuSpmv(a, P.Strategy(P.StrategyKind[name], P.AccumMethod.interval, p=8, dtype=dtype,
+                                          device=local))
+            for _ in range(3):
+                ox.apply_device(xd, yd)
+            otot, oker = ox.time_products(xd, yd, min(args.steps, 50), flush)
+            ox.close()
+            oms = float(np.mean(otot))
+            others[name] = dict(ms_per_step=oms, gflops=flops / (oms / 1e3) / 1e9,
+                                effective_gbs=mb / (oms / 1e3) / 1e9, kernel_ms=float(np.mean(oker)))
         # end to end through the public host API: pinned x -> device, product, y -> pinned host
         xh = torch.from_numpy(x).pin_memory()
         yh = torch.empty_like(xh).pin_memory()
@@ -262,6 +276,7 @@ def main():
         ex.close()
         ms_max = ms
     else:
+        others = {}
         from paper_1003_0952_b200.dist import DistSpmv
         ds = DistSpmv(a, strat)
         p = ds.plan
@@ -324,7 +339,7 @@ def main():
         gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
         roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                       traffic=load_traffic(wl), peak_source=peak_src,
-                      kernel="k_windowed" if args.kind == "windowed" else args.kind,
+                      kernel=f"k_{args.kind}" if args.kind in ("gather", "windowed", "atomic") else args.kind,
                       algorithmic_bytes_per_launch=mb, kernel_ms=kms),
         e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
                  else (p.row_end - p.lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
@@ -332,6 +347,8 @@ def main():
         gpu_launches=launches_per_step * args.steps,
         clocks=clocks,
     )
+    if others:
+        line["kernels"] = others
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         res = cpu_reference(a if args.dtype == "f64" else a, x, 15.0, threads)

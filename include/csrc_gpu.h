@@ -69,7 +69,9 @@ enum {
     CSRC_KIND_LOCAL_BUFFERS = 1,/* windowed kernel into private band buffers + accumulation pass */
     CSRC_KIND_COLORFUL = 2,     /* one launch per conflict-free row class, no atomics */
     CSRC_KIND_ATOMIC = 3,       /* global fp64/fp32 red.global scatter baseline */
-    CSRC_KIND_WINDOWED = 4      /* CTA bands, smem y rings, red.global flush (fastest) */
+    CSRC_KIND_WINDOWED = 4,     /* TMA tiles, smem y rings, red.global flush (CSRC model bytes) */
+    CSRC_KIND_GATHER = 5        /* transposed gather: plan adds the CSR index of the upper
+                                   triangle (+4 B/pair over the CSRC model), no scatter at all */
 };
 
 /* csrc::AccumMethod (parallel.hpp:17) */

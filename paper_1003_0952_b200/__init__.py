@@ -68,6 +68,7 @@ class StrategyKind(enum.IntEnum):
     colorful = 2
     atomic = 3
     windowed = 4
+    gather = 5
 
 
 class AccumMethod(enum.IntEnum):
@@ -505,7 +506,7 @@ def spmv_parallel(a: CsrcMatrix, x, s: Strategy) -> Tuple[np.ndarray, PhaseTimin
 
 
 def spmv_csrc(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarray:
-    """spmv_csrc (kernels.hpp:25-43) on the GPU (windowed kernel)."""
+    """spmv_csrc (kernels.hpp:25-43) on the GPU (gather kernel, deterministic)."""
     xv = _as(x, np.float64)
     if xv.size != a.n:
         raise Error(f"spmv_csrc: x has length {xv.size}, expected {a.n}")

@@ -104,6 +104,11 @@ struct csrc_gpu_plan_s {
     int bands_part[2] = {0, 0};
     DevBuf sched_part[2], cta_ptr_part[2];
 
+    // transposed gather
+    DevBuf uptr, uidx, uval_au, uval_al;
+    int gather_lanes = 4;
+    bool gather_stream = true;
+
     // local buffers
     DevBuf buf, boff, blo, bhi, bstart, iv_begin, iv_end, cptr, contrib;
     int n_iv = 0;
@@ -557,6 +562,70 @@ int pick_lanes(count_t k, index_t n) {
     return 32;
 }
 
+int grid_for(int device, int64_t work, int per_block);
+
+// -------------------------------------------------------------- gather
+// CSR of the upper triangle: for row q the rows r > q with q in ja(r)
+// (ascending), and the au (normal product) / al (transpose) values there.
+template <class T>
+void setup_gather(Plan& P, const MatView& a) {
+    const index_t n = a.n;
+    std::vector<int32_t> uptr(static_cast<size_t>(n) + 1, 0);
+    for (count_t t = 0; t < a.k; ++t) ++uptr[a.ja[t] + 1];
+    for (index_t q = 0; q < n; ++q) uptr[q + 1] += uptr[q];
+    std::vector<int32_t> uidx(static_cast<size_t>(a.k));
+    std::vector<double> vau(static_cast<size_t>(a.k)), val(static_cast<size_t>(a.k));
+    {
+        std::vector<int32_t> next(uptr.begin(), uptr.end() - 1);
+        for (index_t r = 0; r < n; ++r)
+            for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) {
+                const int32_t pos = next[a.ja[t]]++;
+                uidx[pos] = r;
+                vau[pos] = a.au[t];
+                val[pos] = a.al[t];
+            }
+    }
+    const double avg = n ? 2.0 * static_cast<double>(a.k) / n : 0.0;  // off-diagonal entries per row
+    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 32 ? 4 : 8);
+    P.gather_stream = env_int("CSRC_GPU_GSTREAM", 0) != 0;
+    upload(P.uptr, uptr.data(), uptr.size());
+    upload(P.uidx, uidx.data(), uidx.size());
+    upload_values<T>(P.uval_au, vau.data(), vau.size());
+    if (!a.value_symmetric) upload_values<T>(P.uval_al, val.data(), val.size());
+}
+
+template <class T, int L, bool ST>
+void launch_gather_L(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    const T* lo_vals = (tr ? P.au : P.al).template as<T>();
+    const T* up_vals = (tr ? P.uval_al : P.uval_au).template as<T>();
+    if (P.value_symmetric) {
+        lo_vals = P.al.as<T>();
+        up_vals = P.uval_au.as<T>();
+    }
+    dev::k_gather<T, L, ST><<<grid_for(P.device, P.nrows, 256 / L), 256, 0, st>>>(
+        P.ia.as<int32_t>(), P.ja.as<int32_t>(), lo_vals, P.uptr.as<int32_t>(),
+        P.uidx.as<int32_t>(), up_vals, P.ad.as<T>(), x, y, P.nrows);
+}
+
+template <class T, bool ST>
+void launch_gather_S(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    switch (P.gather_lanes) {
+        case 1: launch_gather_L<T, 1, ST>(P, tr, x, y, st); break;
+        case 2: launch_gather_L<T, 2, ST>(P, tr, x, y, st); break;
+        case 8: launch_gather_L<T, 8, ST>(P, tr, x, y, st); break;
+        case 16: launch_gather_L<T, 16, ST>(P, tr, x, y, st); break;
+        default: launch_gather_L<T, 4, ST>(P, tr, x, y, st); break;
+    }
+}
+
+template <class T>
+void launch_gather(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    if (P.gather_stream)
+        launch_gather_S<T, true>(P, tr, x, y, st);
+    else
+        launch_gather_S<T, false>(P, tr, x, y, st);
+}
+
 // -------------------------------------------------------------- creation
 struct CreateOpts {
     const int32_t* color = nullptr;
@@ -626,6 +695,10 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
         case CSRC_KIND_ATOMIC:
             P.launches = 2;
             break;
+        case CSRC_KIND_GATHER:
+            setup_gather<T>(P, a);
+            P.launches = 1;
+            break;
         default:
             throw Error("unknown strategy kind " + std::to_string(P.exec_kind));
     }
@@ -638,7 +711,7 @@ Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const C
     if (s->p < 1) throw Error("ParallelSpmv: thread count must be >= 1");
     if (s->kind == CSRC_KIND_SEQUENTIAL && s->p != 1)
         throw Error("ParallelSpmv: sequential strategy requires p = 1");
-    if (s->kind < CSRC_KIND_SEQUENTIAL || s->kind > CSRC_KIND_WINDOWED)
+    if (s->kind < CSRC_KIND_SEQUENTIAL || s->kind > CSRC_KIND_GATHER)
         throw Error("unknown strategy kind " + std::to_string(s->kind));
     if (s->dtype != CSRC_DTYPE_F64 && s->dtype != CSRC_DTYPE_F32)
         throw Error("unknown dtype " + std::to_string(s->dtype));
@@ -686,12 +759,14 @@ Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const C
         P->row_end = a.n;
         P->lo = 0;
     }
-    // what runs: p = 1 or sequential short-circuit (parallel.hpp:197-202) -> windowed, no buffers
+    // what runs: p = 1 or sequential short-circuit (parallel.hpp:197-202) -> no buffers;
+    // the gather kernel (deterministic, fastest) for whole-matrix plans, windowed for bands
     P->exec_kind = s->kind;
-    if (s->kind == CSRC_KIND_SEQUENTIAL) P->exec_kind = CSRC_KIND_WINDOWED;
-    if (s->kind == CSRC_KIND_LOCAL_BUFFERS && s->p < 2 && !o.block_start)
-        P->exec_kind = CSRC_KIND_WINDOWED;
-    if (o.band && (P->exec_kind == CSRC_KIND_LOCAL_BUFFERS || P->exec_kind == CSRC_KIND_COLORFUL))
+    const int single = o.band ? CSRC_KIND_WINDOWED : CSRC_KIND_GATHER;
+    if (s->kind == CSRC_KIND_SEQUENTIAL) P->exec_kind = single;
+    if (s->kind == CSRC_KIND_LOCAL_BUFFERS && s->p < 2 && !o.block_start) P->exec_kind = single;
+    if (o.band && (P->exec_kind == CSRC_KIND_LOCAL_BUFFERS || P->exec_kind == CSRC_KIND_COLORFUL ||
+                   P->exec_kind == CSRC_KIND_GATHER))
         throw Error("band plans support the windowed and atomic kernels only");
     CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
     for (auto& e : P->ev) CUDA_OK(cudaEventCreate(&e));
@@ -801,6 +876,12 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
             CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
             rec(P, 1, st);
             launch_atomic<T>(P, tr, x, y, st);
+            rec(P, 2, st);
+            break;
+        }
+        case CSRC_KIND_GATHER: {
+            rec(P, 1, st);  // no init: every y element is written once
+            launch_gather<T>(P, tr, x, y, st);
             rec(P, 2, st);
             break;
         }
@@ -998,7 +1079,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.dx, &P.dy, &P.dxd, &P.dyd})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.uptr, &P.uidx, &P.uval_au, &P.uval_al, &P.dx, &P.dy, &P.dxd, &P.dyd})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS

@@ -27,6 +27,7 @@ halo logic on CPU with world size 2.
 """
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Tuple
 
@@ -96,6 +97,10 @@ class DistSpmv:
         self.ex = None
         if band_compute is None:
             s = strategy or Strategy(StrategyKind.windowed)
+            if s.kind == StrategyKind.gather:
+                # the gather kernel reads x above the band (x halo, not y halo);
+                # band plans use the scatter form whose exchange is the y halo
+                s = dataclasses.replace(s, kind=StrategyKind.windowed)
             self.ex = GpuSpmv(a, s, band=(self.plan.row_begin, self.plan.row_end))
             assert self.ex.info().lo == self.plan.lo
         self._bufs = None

@@ -24,6 +24,7 @@ A = P.AccumMethod
 STRATEGIES = [
     ("sequential", P.Strategy(K.sequential)),
     ("windowed", P.Strategy(K.windowed)),
+    ("gather", P.Strategy(K.gather)),
     ("atomic", P.Strategy(K.atomic)),
     ("colorful_nbh", P.Strategy(K.colorful, p=4)),
     ("colorful_exact", P.Strategy(K.colorful, p=4, conflict_mode=P.ConflictMode.exact)),
@@ -69,6 +70,21 @@ def test_family_transpose(idx):
     a = FAM.matrix(p)
     y = P.spmv_csrc_transpose(a, FAM[p + "xr"])
     assert rel_l2(y, FAM[p + "yt"]) <= TOL64
+    for kind in (K.windowed, K.gather, K.atomic, K.colorful):
+        y = run(a, FAM[p + "xr"], P.Strategy(kind, p=2), transpose=True)
+        assert rel_l2(y, FAM[p + "yt"]) <= TOL64, kind.name
+
+
+def test_gather_is_bit_reproducible():
+    """The gather kernel has a fixed summation order per row: repeated
+    products are bit-identical (no atomics anywhere)."""
+    a = MESH.matrix("g5_")
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    y1 = ex.apply(MESH["g5_x"])
+    for _ in range(5):
+        assert np.array_equal(ex.apply(MESH["g5_x"]), y1)
+    assert ex.info().launches_per_apply == 1
+    ex.close()
 
 
 @pytest.mark.parametrize("name,s", STRATEGIES, ids=[n for n, _ in STRATEGIES])
@@ -80,7 +96,7 @@ def test_meshes(name, s, idx):
     assert rel_l2(y, MESH[p + "y"]) <= TOL64
 
 
-@pytest.mark.parametrize("kind", [K.windowed, K.atomic, K.colorful])
+@pytest.mark.parametrize("kind", [K.windowed, K.gather, K.atomic, K.colorful])
 @pytest.mark.parametrize("idx", range(6))
 def test_meshes_fp32(kind, idx):
     p = f"g{idx}_"
@@ -96,6 +112,7 @@ def test_p1_matches_the_reference_path():
     a = MESH.matrix("g1_")
     ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, A.effective, p=1))
     assert ex.buffers_allocated() == 0
+    assert ex.info().launches_per_apply == 1  # runs the gather kernel
     assert rel_l2(ex.apply(MESH["g1_x"]), MESH["g1_y"]) <= TOL64
     ex.close()
     ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, A.effective, p=4))
@@ -205,8 +222,8 @@ def test_device_and_graph_entry_points():
     import torch
     a, x, _ = P.config_matrix("c1")
     ref = O.spmv_csrc(a, x)
-    for s in (P.Strategy(K.windowed), P.Strategy(K.atomic), P.Strategy(K.colorful, p=2),
-              P.Strategy(K.local_buffers, A.effective, p=2)):
+    for s in (P.Strategy(K.windowed), P.Strategy(K.gather), P.Strategy(K.atomic),
+              P.Strategy(K.colorful, p=2), P.Strategy(K.local_buffers, A.effective, p=2)):
         ex = P.GpuSpmv(a, s)
         xd = torch.from_numpy(x).cuda()
         yd = torch.full_like(xd, float("nan"))
@@ -223,7 +240,7 @@ def test_device_and_graph_entry_points():
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
-@pytest.mark.parametrize("kind", [K.windowed, K.atomic, K.colorful, K.local_buffers])
+@pytest.mark.parametrize("kind", [K.windowed, K.gather, K.atomic, K.colorful, K.local_buffers])
 def test_configs_full_size(cfg, kind):
     a, x, _ = P.config_matrix(cfg)
     ref = O.spmv_csrc(a, x)
@@ -231,26 +248,28 @@ def test_configs_full_size(cfg, kind):
     assert rel_l2(y, ref) <= TOL64 and rel_inf(y, ref) <= TOL64
 
 
+@pytest.mark.parametrize("kind", [K.windowed, K.gather])
 @pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
-def test_large_configs_windowed(cfg):
+def test_large_configs(cfg, kind):
     a, x, _ = P.config_matrix(cfg)
     ref = O.spmv_csrc(a, x)
-    y = run(a, x, P.Strategy(K.windowed))
+    y = run(a, x, P.Strategy(kind))
     assert rel_l2(y, ref) <= TOL64
     # linearity, a size-independent property: A(x + 2 z) = A x + 2 A z
     z = np.random.default_rng(1).uniform(-1, 1, a.n)
-    ex = P.GpuSpmv(a, P.Strategy(K.windowed))
+    ex = P.GpuSpmv(a, P.Strategy(kind))
     lhs = ex.apply(x + 2 * z)
     rhs = ex.apply(x) + 2 * ex.apply(z)
     assert rel_l2(lhs, rhs) <= 1e-13
     ex.close()
 
 
-def test_c5_fp32():
+@pytest.mark.parametrize("kind", [K.windowed, K.gather])
+def test_c5_fp32(kind):
     a, x, _ = P.config_matrix("c5")
     x32 = x.astype(np.float32).astype(np.float64)
     ref = O.spmv_csrc(round32(a), x32)
-    y = run(a, x32, P.Strategy(K.windowed, dtype=P.DType.f32))
+    y = run(a, x32, P.Strategy(kind, dtype=P.DType.f32))
     assert rel_l2(y, ref) <= TOL32
 
 

@@ -7,7 +7,7 @@ import paper_1003_0952_b200 as P
 from oracle.oracle import Oracle, rel_l2
 O = Oracle()
 cfgs = sys.argv[1].split(',') if len(sys.argv) > 1 else ['c1', 'c2']
-kinds = [('windowed', P.StrategyKind.windowed, 0), ('atomic', P.StrategyKind.atomic, 0),
+kinds = [('windowed', P.StrategyKind.windowed, 0), ('gather', P.StrategyKind.gather, 0), ('atomic', P.StrategyKind.atomic, 0),
          ('colorful', P.StrategyKind.colorful, 0), ('lb_effective', P.StrategyKind.local_buffers, 2),
          ('lb_interval', P.StrategyKind.local_buffers, 3), ('lb_all_in_one', P.StrategyKind.local_buffers, 0),
          ('lb_per_buffer', P.StrategyKind.local_buffers, 1)]
