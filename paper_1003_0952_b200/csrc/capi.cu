@@ -104,10 +104,22 @@ struct csrc_gpu_plan_s {
     int bands_part[2] = {0, 0};
     DevBuf sched_part[2], cta_ptr_part[2];
 
-    // transposed gather
-    DevBuf uptr, uidx, uval_au, uval_al;
-    int gather_lanes = 4;
-    bool gather_stream = true;
+    // transposed gather: interleaved entry stream (gather.cuh), row tiles,
+    // rows longer than a stage
+    DevBuf eptr, eidx, eval, eval_t;
+    int gather_lanes = 4;  // lanes per row (k_gather_rows)
+    int gather_pf = 2;     // L2 prefetch distance in block iterations (0 = off)
+    int gather_bpsm = 16;  // resident-grid cap: blocks per SM
+    int gather_buf = 0;    // k_gather_buf with U = gather_u (0: k_gather_rows)
+    int gather_u = 8;
+    int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
+    int gather_grid = 0;
+    // host-API pipeline (apply_host): row chunks, and for each the last x chunk it reads
+    std::vector<int32_t> hchunk;
+    std::vector<int32_t> hneed;
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_in = nullptr;
+    std::vector<cudaEvent_t> ev_x, ev_y;
 
     // local buffers
     DevBuf buf, boff, blo, bhi, bstart, iv_begin, iv_end, cptr, contrib;
@@ -141,6 +153,12 @@ struct csrc_gpu_plan_s {
         if (graph) cudaGraphExecDestroy(graph);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
+        for (auto* v : {&ev_x, &ev_y})
+            for (auto& e : *v)
+                if (e) cudaEventDestroy(e);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (s_h2d) cudaStreamDestroy(s_h2d);
+        if (s_d2h) cudaStreamDestroy(s_d2h);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -565,65 +583,168 @@ int pick_lanes(count_t k, index_t n) {
 int grid_for(int device, int64_t work, int per_block);
 
 // -------------------------------------------------------------- gather
-// CSR of the upper triangle: for row q the rows r > q with q in ja(r)
-// (ascending), and the au (normal product) / al (transpose) values there.
+// Entry stream per row q: lower pairs of q (ja / al, CSRC order), then the
+// pairs (r, q), r > q ascending, with their au (normal product) or al
+// (transpose) value. eval_t only exists for value-unsymmetric matrices.
+template <class T>
+int gather_buf_smem(const Plan& P) {
+    return 16 + 2 * (dev::gather_idx_bytes(P.gather_cap) + dev::gather_val_bytes<T>(P.gather_cap));
+}
+
+template <class T, int U>
+void* gather_buf_fn_U(int L) {
+    switch (L) {
+        case 1: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 1, U>);
+        case 2: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 2, U>);
+        case 8: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 8, U>);
+        case 16: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 16, U>);
+        default: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 4, U>);
+    }
+}
+
+template <class T>
+void* gather_buf_fn(int L, int U) {
+    return U == 4 ? gather_buf_fn_U<T, 4>(L) : gather_buf_fn_U<T, 8>(L);
+}
+
 template <class T>
 void setup_gather(Plan& P, const MatView& a) {
     const index_t n = a.n;
-    std::vector<int32_t> uptr(static_cast<size_t>(n) + 1, 0);
-    for (count_t t = 0; t < a.k; ++t) ++uptr[a.ja[t] + 1];
-    for (index_t q = 0; q < n; ++q) uptr[q + 1] += uptr[q];
-    std::vector<int32_t> uidx(static_cast<size_t>(a.k));
-    std::vector<double> vau(static_cast<size_t>(a.k)), val(static_cast<size_t>(a.k));
+    if (2 * static_cast<int64_t>(a.k) > INT32_MAX)
+        throw Error("gather plan: more than 2^31 off-diagonal entries (use the windowed kernel)");
+    std::vector<int32_t> up(static_cast<size_t>(n) + 1, 0);
+    for (count_t t = 0; t < a.k; ++t) ++up[a.ja[t] + 1];
+    std::vector<int32_t> eptr(static_cast<size_t>(n) + 1, 0);
+    for (index_t q = 0; q < n; ++q)
+        eptr[q + 1] = eptr[q] + (a.ia[q + 1] - a.ia[q]) + up[q + 1];
+    const size_t ne = static_cast<size_t>(eptr[n]);
+    std::vector<int32_t> eidx(ne);
+    std::vector<double> ev(ne), evt(a.value_symmetric ? 0 : ne);
+    std::vector<int32_t> next(static_cast<size_t>(n));
+    for (index_t q = 0; q < n; ++q) {
+        int32_t w = eptr[q];
+        for (index_t t = a.ia[q]; t < a.ia[q + 1]; ++t, ++w) {
+            eidx[w] = a.ja[t];
+            ev[w] = a.al[t];
+            if (!a.value_symmetric) evt[w] = a.au[t];
+        }
+        next[q] = w;  // upper entries of q start here
+    }
+    for (index_t r = 0; r < n; ++r)  // ascending r: upper entries land sorted
+        for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) {
+            const int32_t w = next[a.ja[t]]++;
+            eidx[w] = r;
+            ev[w] = a.value_symmetric ? a.al[t] : a.au[t];
+            if (!a.value_symmetric) evt[w] = a.al[t];
+        }
+    upload(P.eptr, eptr.data(), eptr.size());
+    upload(P.eidx, eidx.data(), eidx.size());
+    upload_values<T>(P.eval, ev.data(), ev.size());
+    if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
+
+    const double avg = n ? static_cast<double>(ne) / n : 0.0;
+    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 10 ? 2 : avg <= 128 ? 4 : 8);
+    P.gather_pf = env_int("CSRC_GPU_GPF", 0);
+    P.gather_bpsm = env_int("CSRC_GPU_GBPSM", 16);  // 256-thread blocks per SM
     {
-        std::vector<int32_t> next(uptr.begin(), uptr.end() - 1);
-        for (index_t r = 0; r < n; ++r)
-            for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) {
-                const int32_t pos = next[a.ja[t]]++;
-                uidx[pos] = r;
-                vau[pos] = a.au[t];
-                val[pos] = a.al[t];
+        // host pipeline: C row chunks on multiples of 256 rows (any lane count's block)
+        const int64_t want = std::max<int64_t>(1, std::min<int64_t>(env_int("CSRC_GPU_HOST_CHUNKS", 16), n / (1 << 18)));
+        const int64_t step = ((n + want - 1) / want + 255) / 256 * 256;
+        P.hchunk.clear();
+        for (int64_t r = 0; r < n; r += step) P.hchunk.push_back(static_cast<int32_t>(r));
+        P.hchunk.push_back(n);
+        const int nc = static_cast<int>(P.hchunk.size()) - 1;
+        P.hneed.assign(nc, 0);
+        for (int c = 0; c < nc; ++c) {
+            int32_t hi = P.hchunk[c + 1] - 1;  // the diagonal reads x[row]
+            for (int64_t e = eptr[P.hchunk[c]]; e < eptr[P.hchunk[c + 1]]; ++e) hi = std::max(hi, eidx[e]);
+            // chunk holding column hi
+            P.hneed[c] = static_cast<int32_t>(std::upper_bound(P.hchunk.begin(), P.hchunk.end() - 1, hi) -
+                                              P.hchunk.begin()) - 1;
+        }
+    }
+    // double-buffered form: needs the largest row-block span to fit twice in shared memory
+    P.gather_u = env_int("CSRC_GPU_GU", 8) == 4 ? 4 : 8;
+    if (env_int("CSRC_GPU_GBUF", 1) != 0) {
+        const int R = 256 / P.gather_lanes;
+        int64_t cap = 0;
+        for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
+        const int64_t bytes = 16 + 2 * (((cap + 8) * 4 + 15) / 16 * 16 + ((cap + 8) * static_cast<int64_t>(sizeof(T)) + 15) / 16 * 16);
+        if (bytes <= 100 * 1024) {
+            P.gather_cap = static_cast<int>(cap);
+            void* fn = gather_buf_fn<T>(P.gather_lanes, P.gather_u);
+            const int smem = gather_buf_smem<T>(P);
+            CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            int occ = 0;
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+            if (occ >= 1) {
+                P.gather_buf = 1;
+                const int64_t blocks = (n + R - 1) / R;
+                P.gather_grid = static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(num_sms(P.device)) * occ));
             }
+        }
     }
-    const double avg = n ? 2.0 * static_cast<double>(a.k) / n : 0.0;  // off-diagonal entries per row
-    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 32 ? 4 : 8);
-    P.gather_stream = env_int("CSRC_GPU_GSTREAM", 0) != 0;
-    upload(P.uptr, uptr.data(), uptr.size());
-    upload(P.uidx, uidx.data(), uidx.size());
-    upload_values<T>(P.uval_au, vau.data(), vau.size());
-    if (!a.value_symmetric) upload_values<T>(P.uval_al, val.data(), val.size());
 }
 
-template <class T, int L, bool ST>
-void launch_gather_L(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
-    const T* lo_vals = (tr ? P.au : P.al).template as<T>();
-    const T* up_vals = (tr ? P.uval_al : P.uval_au).template as<T>();
-    if (P.value_symmetric) {
-        lo_vals = P.al.as<T>();
-        up_vals = P.uval_au.as<T>();
-    }
-    dev::k_gather<T, L, ST><<<grid_for(P.device, P.nrows, 256 / L), 256, 0, st>>>(
-        P.ia.as<int32_t>(), P.ja.as<int32_t>(), lo_vals, P.uptr.as<int32_t>(),
-        P.uidx.as<int32_t>(), up_vals, P.ad.as<T>(), x, y, P.nrows);
+template <class T, int L, int PF>
+void launch_gather_rows_LP(const Plan& P, const T* vals, const T* x, T* y, const int32_t* rows,
+                           int32_t row0, int32_t count, cudaStream_t st) {
+    const int64_t blocks = (static_cast<int64_t>(count) + 256 / L - 1) / (256 / L);
+    const int64_t cap = static_cast<int64_t>(num_sms(P.device)) * std::max(1, P.gather_bpsm);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min(blocks, cap)));
+    dev::k_gather_rows<T, L, PF><<<grid, 256, 0, st>>>(P.eptr.as<int32_t>(), P.eidx.as<int32_t>(),
+                                                       vals, P.ad.as<T>(), x, y, rows, row0, count);
 }
 
-template <class T, bool ST>
-void launch_gather_S(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+template <class T, int L>
+void launch_gather_rows_L(const Plan& P, const T* vals, const T* x, T* y, int32_t r0, int32_t r1,
+                          cudaStream_t st) {
+    switch (P.gather_pf) {
+        case 0: launch_gather_rows_LP<T, L, 0>(P, vals, x, y, nullptr, r0, r1 - r0, st); break;
+        case 1: launch_gather_rows_LP<T, L, 1>(P, vals, x, y, nullptr, r0, r1 - r0, st); break;
+        case 4: launch_gather_rows_LP<T, L, 4>(P, vals, x, y, nullptr, r0, r1 - r0, st); break;
+        default: launch_gather_rows_LP<T, L, 2>(P, vals, x, y, nullptr, r0, r1 - r0, st); break;
+    }
+}
+
+// rows [r0, r1) of the gather product (r0 a multiple of 256 / lanes unless 0)
+template <class T>
+void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, int32_t r1,
+                         cudaStream_t st) {
+    if (r1 <= r0) return;
+    const T* vals = (tr && !P.value_symmetric ? P.eval_t : P.eval).template as<T>();
+    if (P.gather_buf) {
+        const int R = 256 / P.gather_lanes;
+        dev::GBufArgs<T> A;
+        A.eptr = P.eptr.as<int32_t>();
+        A.eidx = P.eidx.as<int32_t>();
+        A.eval = vals;
+        A.ad = P.ad.as<T>();
+        A.x = x;
+        A.y = y;
+        A.row0 = r0;
+        A.nrows = r1;
+        A.idx_bytes = dev::gather_idx_bytes(P.gather_cap);
+        A.val_bytes = dev::gather_val_bytes<T>(P.gather_cap);
+        const int64_t blocks = (static_cast<int64_t>(r1 - r0) + R - 1) / R;
+        const int grid = static_cast<int>(std::min<int64_t>(blocks, P.gather_grid));
+        void* args[] = {&A};
+        CUDA_OK(cudaLaunchKernel(gather_buf_fn<T>(P.gather_lanes, P.gather_u), dim3(grid), dim3(256),
+                                 args, static_cast<size_t>(gather_buf_smem<T>(P)), st));
+        return;
+    }
     switch (P.gather_lanes) {
-        case 1: launch_gather_L<T, 1, ST>(P, tr, x, y, st); break;
-        case 2: launch_gather_L<T, 2, ST>(P, tr, x, y, st); break;
-        case 8: launch_gather_L<T, 8, ST>(P, tr, x, y, st); break;
-        case 16: launch_gather_L<T, 16, ST>(P, tr, x, y, st); break;
-        default: launch_gather_L<T, 4, ST>(P, tr, x, y, st); break;
+        case 1: launch_gather_rows_L<T, 1>(P, vals, x, y, r0, r1, st); break;
+        case 2: launch_gather_rows_L<T, 2>(P, vals, x, y, r0, r1, st); break;
+        case 8: launch_gather_rows_L<T, 8>(P, vals, x, y, r0, r1, st); break;
+        case 16: launch_gather_rows_L<T, 16>(P, vals, x, y, r0, r1, st); break;
+        default: launch_gather_rows_L<T, 4>(P, vals, x, y, r0, r1, st); break;
     }
 }
 
 template <class T>
 void launch_gather(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
-    if (P.gather_stream)
-        launch_gather_S<T, true>(P, tr, x, y, st);
-    else
-        launch_gather_S<T, false>(P, tr, x, y, st);
+    launch_gather_range<T>(P, tr, x, y, 0, P.nrows, st);
 }
 
 // -------------------------------------------------------------- creation
@@ -652,12 +773,13 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
         upload(P.ia, ia_loc.data(), ia_loc.size());
     }
     const bool colored = P.exec_kind == CSRC_KIND_COLORFUL;
-    if (!colored) {
+    const bool gather = P.exec_kind == CSRC_KIND_GATHER;  // keeps its own entry stream
+    if (!colored && !gather) {
         upload(P.ja, a.ja + t0, static_cast<size_t>(P.k));
         upload_values<T>(P.al, a.al + t0, static_cast<size_t>(P.k));
         if (!a.value_symmetric) upload_values<T>(P.au, a.au + t0, static_cast<size_t>(P.k));
-        upload_values<T>(P.ad, a.ad + r0, static_cast<size_t>(P.nrows));
     }
+    if (!colored) upload_values<T>(P.ad, a.ad + r0, static_cast<size_t>(P.nrows));
     switch (P.exec_kind) {
         case CSRC_KIND_WINDOWED: {
             std::vector<index_t> bs;
@@ -954,6 +1076,69 @@ void apply_device(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, i
         apply_typed<float>(P, dx, dy, st, tr, part);
 }
 
+// Host product with the copies overlapped (gather plans): x goes up in row
+// chunks on s_h2d; chunk c's rows run on the compute stream once the last x
+// chunk they read (hneed[c], plan time) has landed; its y rows go down on
+// s_d2h while later chunks compute. H2D and D2H use the two copy directions
+// of the link concurrently. Same kernels and summation order as the device
+// entry point, so results are bit-identical to it.
+void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
+    const int nc = static_cast<int>(P.hchunk.size()) - 1;
+    if (!P.s_h2d) {
+        CUDA_OK(cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreateWithFlags(&P.ev_in, cudaEventDisableTiming));
+        P.ev_x.assign(nc, nullptr);
+        P.ev_y.assign(nc, nullptr);
+        for (int c = 0; c < nc; ++c) {
+            CUDA_OK(cudaEventCreateWithFlags(&P.ev_x[c], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&P.ev_y[c], cudaEventDisableTiming));
+        }
+    }
+    const bool f32 = P.dtype == CSRC_DTYPE_F32;
+    if (f32) {
+        const size_t n = static_cast<size_t>(P.n_global);
+        if (!P.dxd.p) P.dxd.alloc(n * 8);
+        if (!P.dyd.p) P.dyd.alloc(n * 8);
+    }
+    double* xd64 = f32 ? P.dxd.as<double>() : P.dx.as<double>();
+    double* yd64 = f32 ? P.dyd.as<double>() : P.dy.as<double>();
+    cudaStream_t st = P.stream;
+    CUDA_OK(cudaEventRecord(P.ev_in, st));
+    CUDA_OK(cudaStreamWaitEvent(P.s_h2d, P.ev_in, 0));  // after earlier work on the plan stream
+    for (int c = 0; c < nc; ++c) {
+        const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
+        CUDA_OK(cudaMemcpyAsync(xd64 + r0, xh + r0, len * 8, cudaMemcpyHostToDevice, P.s_h2d));
+        CUDA_OK(cudaEventRecord(P.ev_x[c], P.s_h2d));
+    }
+    int have = -1;  // x chunks the compute stream already waited for (and converted)
+    for (int c = 0; c < nc; ++c) {
+        for (; have < P.hneed[c]; ++have) {
+            CUDA_OK(cudaStreamWaitEvent(st, P.ev_x[have + 1], 0));
+            if (f32) {
+                const int32_t a = P.hchunk[have + 1], b = P.hchunk[have + 2];
+                dev::k_convert<double, float><<<grid_for(P.device, b - a, 256), 256, 0, st>>>(
+                    P.dxd.as<double>() + a, P.dx.as<float>() + a, b - a);
+            }
+        }
+        const int32_t r0 = P.hchunk[c], r1 = P.hchunk[c + 1];
+        if (f32) {
+            launch_gather_range<float>(P, tr, P.dx.as<float>(), P.dy.as<float>(), r0, r1, st);
+            dev::k_convert<float, double><<<grid_for(P.device, r1 - r0, 256), 256, 0, st>>>(
+                P.dy.as<float>() + r0, P.dyd.as<double>() + r0, r1 - r0);
+        } else {
+            launch_gather_range<double>(P, tr, P.dx.as<double>(), P.dy.as<double>(), r0, r1, st);
+        }
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaEventRecord(P.ev_y[c], st));
+        CUDA_OK(cudaStreamWaitEvent(P.s_d2h, P.ev_y[c], 0));
+        CUDA_OK(cudaMemcpyAsync(yh + r0, yd64 + r0, static_cast<size_t>(r1 - r0) * 8,
+                                cudaMemcpyDeviceToHost, P.s_d2h));
+    }
+    CUDA_OK(cudaStreamSynchronize(P.s_d2h));
+    CUDA_OK(cudaStreamSynchronize(st));
+}
+
 void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
     if (x_len != P.n_global)
         throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +
@@ -966,6 +1151,10 @@ void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
     if (!P.dx.p) P.dx.alloc(n * P.vsize());
     if (!P.dy.p) P.dy.alloc(n * P.vsize());
     cudaStream_t st = P.stream;
+    if (P.exec_kind == CSRC_KIND_GATHER && P.hchunk.size() > 2 && !P.timing) {
+        apply_host_pipelined(P, xh, yh, tr);
+        return;
+    }
     if (P.dtype == CSRC_DTYPE_F64) {
         CUDA_OK(cudaMemcpyAsync(P.dx.p, xh, n * 8, cudaMemcpyHostToDevice, st));
         apply_device(P, P.dx.p, P.dy.p, st, tr);
@@ -1079,7 +1268,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.uptr, &P.uidx, &P.uval_au, &P.uval_al, &P.dx, &P.dy, &P.dxd, &P.dyd})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.dx, &P.dy, &P.dxd, &P.dyd})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS

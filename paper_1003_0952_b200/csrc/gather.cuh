@@ -1,0 +1,217 @@
+// Transposed-gather CSRC product: y_q = ad_q x_q + sum over the row's stored
+// lower pairs (al, ja) + sum over the pairs that name q as their column
+// (the "upper" entries a_{q,r} = au[t] for t in row r with ja[t] = q).
+//
+// The plan (capi.cu setup_gather) lays both parts of each row out as ONE
+// contiguous entry stream: eptr[q] .. eptr[q+1] holds the lower entries of q
+// (ja / al, in CSRC order) followed by its upper entries (ascending r). No
+// scatter, no atomics, no memset: each y element is written exactly once
+// with a fixed summation order (bit-reproducible).
+//
+// k_gather_rows: L lanes per row, grid-stride over row blocks. At full
+// occupancy (<= 32 registers) the loads one warp keeps in flight are too few
+// to cover HBM latency (Little's law: ~49 KB per SM at 64 warps), so thread 0
+// of each block issues a TMA bulk L2 prefetch (cp.async.bulk.prefetch.L2,
+// no registers, no shared memory) of the eidx / eval spans the block will
+// read PF iterations later; the demand loads then hit L2.
+// (A warp-specialised variant that staged row tiles in shared memory and
+// walked them one row per lane lost 1.2-6x: shared memory holds ~700 rows,
+// too few independent x gathers per SM; profiles/r01_sweep_gather_staged.txt.)
+#pragma once
+
+#include <cstdint>
+
+namespace csrcgpu {
+namespace dev {
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// 16-byte aligned span covering elements [i0, i1) of a
+template <typename E>
+__device__ __forceinline__ void prefetch_span(const E* a, int64_t i0, int64_t i1) {
+    if (i1 <= i0) return;
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(a + i0) & ~uintptr_t(15);
+    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(a + i1) + 15) & ~uintptr_t(15);
+    prefetch_l2(reinterpret_cast<const void*>(b0), static_cast<uint32_t>(b1 - b0));
+}
+
+// L lanes per row from global memory; rows = rows[0..count) when `rows` is
+// given, else row0 .. row0 + count - 1.
+template <typename T, int L, int PF>
+__global__ void __launch_bounds__(256) k_gather_rows(const int32_t* __restrict__ eptr,
+                                                     const int32_t* __restrict__ eidx,
+                                                     const T* __restrict__ eval,
+                                                     const T* __restrict__ ad,
+                                                     const T* __restrict__ x, T* __restrict__ y,
+                                                     const int32_t* __restrict__ rows,
+                                                     int32_t row0, int32_t count) {
+    const int sub = threadIdx.x % L;
+    const int per_block = blockDim.x / L;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * per_block;
+    if (PF > 0 && rows == nullptr && threadIdx.x == 0) {
+        // warm-up: the first PF iterations' spans
+        for (int d = 0; d < PF; ++d) {
+            const int64_t f0 = static_cast<int64_t>(blockIdx.x) * per_block + d * stride;
+            if (f0 >= count) break;
+            const int64_t f1 = f0 + per_block < count ? f0 + per_block : count;
+            const int32_t e0 = __ldg(eptr + row0 + f0), e1 = __ldg(eptr + row0 + f1);
+            prefetch_span(eidx, e0, e1);
+            prefetch_span(eval, e0, e1);
+        }
+    }
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * per_block; base < count; base += stride) {
+        if (PF > 0 && rows == nullptr && threadIdx.x == 0) {
+            const int64_t f0 = base + PF * stride;
+            if (f0 < count) {
+                const int64_t f1 = f0 + per_block < count ? f0 + per_block : count;
+                const int32_t e0 = __ldg(eptr + row0 + f0), e1 = __ldg(eptr + row0 + f1);
+                prefetch_span(eidx, e0, e1);
+                prefetch_span(eval, e0, e1);
+            }
+        }
+        const int64_t i = base + threadIdx.x / L;
+        const bool act = i < count;
+        T s = T(0);
+        int32_t r = 0;
+        if (act) {
+            r = rows ? __ldg(rows + i) : row0 + static_cast<int32_t>(i);
+            const int32_t e0 = __ldg(eptr + r), e1 = __ldg(eptr + r + 1);
+            T s2 = T(0);
+            int32_t e = e0 + sub;
+            for (; e + L < e1; e += 2 * L) {
+                s = fma(__ldg(eval + e), __ldg(x + __ldg(eidx + e)), s);
+                s2 = fma(__ldg(eval + e + L), __ldg(x + __ldg(eidx + e + L)), s2);
+            }
+            if (e < e1) s = fma(__ldg(eval + e), __ldg(x + __ldg(eidx + e)), s);
+            s += s2;
+        }
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
+        if (act && sub == 0) y[r] = s + __ldg(ad + r) * __ldg(x + r);
+    }
+}
+
+// Double-buffered form: each 256-thread block walks row blocks of R = 256 / L
+// rows; thread 0 stages the NEXT row block's eidx / eval spans into shared
+// memory with two cp.async.bulk copies (mbarrier completion) while the block
+// computes the current one. A lane then issues all U gathers of x for its
+// entries back to back from shared-memory indices, so a row costs one global
+// round trip instead of one per entry pair. cap = largest entry span of any
+// row block (plan time).
+// shared-memory bytes of one buffer holding up to `cap` entries (+ alignment slack)
+__host__ __device__ inline int gather_idx_bytes(int cap) { return ((cap + 8) * 4 + 15) & ~15; }
+template <typename T>
+__host__ __device__ inline int gather_val_bytes(int cap) {
+    return ((cap + 8) * static_cast<int>(sizeof(T)) + 15) & ~15;
+}
+
+template <typename T>
+struct GBufArgs {
+    const int32_t* eptr;
+    const int32_t* eidx;
+    const T* eval;
+    const T* ad;
+    const T* x;
+    T* y;
+    int32_t row0;       // rows [row0, nrows); row0 a multiple of R
+    int32_t nrows;
+    int32_t idx_bytes;  // per buffer, 16-aligned, >= 4 * (cap + 8)
+    int32_t val_bytes;  // per buffer, 16-aligned, >= sizeof(T) * (cap + 8)
+};
+
+template <typename T, int L, int U>
+__global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int R = 256 / L;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2]
+    unsigned char* bufs = smem + 16;
+    const int buf_bytes = A.idx_bytes + A.val_bytes;
+    const int sub = threadIdx.x % L;
+    const int rrel = threadIdx.x / L;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * R;
+    const int64_t first = A.row0 + static_cast<int64_t>(blockIdx.x) * R;
+    // thread 0: entry span of the row block two iterations ahead (register pipeline)
+    int32_t nx0 = 0, nx1 = 0;
+    auto span = [&](int64_t b, int32_t& e0, int32_t& e1) {
+        if (b < A.nrows) {
+            e0 = __ldg(A.eptr + b);
+            e1 = __ldg(A.eptr + (b + R < A.nrows ? b + R : A.nrows));
+        }
+    };
+    auto issue = [&](int buf, int32_t e0, int32_t e1) {
+        const Seg<int32_t> si = seg(A.eidx, e0, e1);
+        const Seg<T> sv = seg(A.eval, e0, e1);
+        unsigned char* st = bufs + buf * buf_bytes;
+        mbar_expect_tx(&full[buf], si.bytes + sv.bytes);
+        tma_load(st, si.src, si.bytes, &full[buf]);
+        tma_load(st + A.idx_bytes, sv.src, sv.bytes, &full[buf]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (first < A.nrows) {
+            int32_t e0 = 0, e1 = 0;
+            span(first, e0, e1);
+            issue(0, e0, e1);
+        }
+        span(first + stride, nx0, nx1);
+    }
+    __syncthreads();
+    constexpr int kIdxAlign = 4;
+    constexpr int kValAlign = 16 / sizeof(T);
+    int it = 0;
+    for (int64_t base = first; base < A.nrows; base += stride, ++it) {
+        const int buf = it & 1;
+        if (threadIdx.x == 0 && base + stride < A.nrows) {
+            issue(buf ^ 1, nx0, nx1);  // buffer buf^1 was released by the last __syncthreads
+            span(base + 2 * stride, nx0, nx1);
+        }
+        const int64_t row = base + rrel;
+        const bool act = row < A.nrows;
+        int32_t eb = 0, ee = 0;
+        T d = T(0), xr = T(0);
+        if (act) {
+            eb = __ldg(A.eptr + row);
+            ee = __ldg(A.eptr + row + 1);
+            d = __ldg(A.ad + row);
+            xr = __ldg(A.x + row);
+        }
+        const int32_t e_base = __ldg(A.eptr + base);  // the block's first entry
+        mbar_wait(&full[buf], (it >> 1) & 1);
+        const uint32_t st = smem_u32(bufs + buf * buf_bytes);
+        const uint32_t ib = st - 4u * static_cast<uint32_t>(e_base & ~(kIdxAlign - 1));
+        const uint32_t vb = st + A.idx_bytes -
+                            static_cast<uint32_t>(sizeof(T)) * static_cast<uint32_t>(e_base & ~(kValAlign - 1));
+        T acc0 = T(0), acc1 = T(0);
+        for (int32_t e = eb + sub; e < ee; e += U * L) {
+            T xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t f = e + u * L;
+                xv[u] = T(0);
+                if (f < ee) xv[u] = __ldg(A.x + lds_i(ib + 4u * f));
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int32_t f = e + u * L;
+                if (f < ee) {
+                    if (u & 1)
+                        acc1 = fma(lds_f(vb + sizeof(T) * f, T()), xv[u], acc1);
+                    else
+                        acc0 = fma(lds_f(vb + sizeof(T) * f, T()), xv[u], acc0);
+                }
+            }
+        }
+        T s = acc0 + acc1;
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
+        if (act && sub == 0) A.y[row] = s + d * xr;
+        __syncthreads();
+    }
+}
+
+}  // namespace dev
+}  // namespace csrcgpu

@@ -76,61 +76,6 @@ __global__ void __launch_bounds__(256) k_atomic(const int32_t* __restrict__ ia,
 // matching au values), so y_q = ad_q x_q + sum_lower al x[ja] + sum_upper
 // uval x[uidx] is a pure gather: every y element is written once, no
 // atomics, no zero-init, bit-reproducible.
-template <bool STREAM, typename E>
-__device__ __forceinline__ E ldx(const E* p) {
-    return STREAM ? __ldcs(p) : __ldg(p);
-}
-
-template <typename T, int L, bool STREAM>
-__global__ void __launch_bounds__(256) k_gather(const int32_t* __restrict__ ia,
-                                                const int32_t* __restrict__ ja,
-                                                const T* __restrict__ al,
-                                                const int32_t* __restrict__ uptr,
-                                                const int32_t* __restrict__ uidx,
-                                                const T* __restrict__ uval,
-                                                const T* __restrict__ ad,
-                                                const T* __restrict__ x, T* __restrict__ y,
-                                                int32_t nrows) {
-    const int sub = threadIdx.x % L;
-    const int rows_per_block = blockDim.x / L;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * rows_per_block; base < nrows;
-         base += static_cast<int64_t>(gridDim.x) * rows_per_block) {
-        const int64_t r = base + threadIdx.x / L;
-        const bool act = r < nrows;
-        T s = T(0);
-        if (act) {
-            // one index space [0, nl + nu): lower entries then upper entries,
-            // each contiguous, walked by the L lanes together (no half-empty
-            // iteration between the two parts), two accumulators for ILP
-            const int32_t l0 = __ldg(ia + r), nl = __ldg(ia + r + 1) - l0;
-            const int32_t u0 = __ldg(uptr + r), nu = __ldg(uptr + r + 1) - u0;
-            const int32_t tot = nl + nu;
-            T s2 = T(0);
-            int32_t e = sub;
-            for (; e + L < tot; e += 2 * L) {
-                const int32_t e2 = e + L;
-                const bool lo1 = e < nl, lo2 = e2 < nl;
-                const int32_t c1 = lo1 ? ldx<STREAM>(ja + l0 + e) : ldx<STREAM>(uidx + u0 + e - nl);
-                const int32_t c2 = lo2 ? ldx<STREAM>(ja + l0 + e2) : ldx<STREAM>(uidx + u0 + e2 - nl);
-                const T v1 = lo1 ? ldx<STREAM>(al + l0 + e) : ldx<STREAM>(uval + u0 + e - nl);
-                const T v2 = lo2 ? ldx<STREAM>(al + l0 + e2) : ldx<STREAM>(uval + u0 + e2 - nl);
-                s = fma(v1, __ldg(x + c1), s);
-                s2 = fma(v2, __ldg(x + c2), s2);
-            }
-            if (e < tot) {
-                const bool lo1 = e < nl;
-                const int32_t c1 = lo1 ? ldx<STREAM>(ja + l0 + e) : ldx<STREAM>(uidx + u0 + e - nl);
-                const T v1 = lo1 ? ldx<STREAM>(al + l0 + e) : ldx<STREAM>(uval + u0 + e - nl);
-                s = fma(v1, __ldg(x + c1), s);
-            }
-            s += s2;
-        }
-#pragma unroll
-        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
-        if (act && sub == 0) y[r] = s + ldx<STREAM>(ad + r) * __ldg(x + r);
-    }
-}
-
 // ---------------------------------------------------------------- colored
 // One class per launch (colorful_worker, parallel.hpp:411-434): rows of a
 // class share no written y position, so y[j] += and y[i] += are plain
@@ -176,6 +121,7 @@ __global__ void __launch_bounds__(256) k_colored(const int32_t* __restrict__ rid
 }  // namespace csrcgpu
 
 #include "windowed.cuh"
+#include "gather.cuh"
 
 namespace csrcgpu {
 namespace dev {

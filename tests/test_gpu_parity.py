@@ -303,3 +303,25 @@ def test_band_plans_assemble_the_product(bands, mesh):
         assert ex.band_split() >= r0
         ex.close()
     assert rel_l2(y, MESH[mesh + "y"]) <= TOL64
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_host_pipeline_matches_device(cfg):
+    """The host entry point of a gather plan overlaps the x upload, the row
+    chunks and the y download (capi.cu apply_host_pipelined); it must give
+    exactly the device entry point's result (same kernels, same order)."""
+    import torch
+    a, x, _ = P.config_matrix(cfg)
+    ref = O.spmv_csrc(a, x)
+    for dt, tdt in ((P.DType.f64, torch.float64), (P.DType.f32, torch.float32)):
+        ex = P.GpuSpmv(a, P.Strategy(K.gather, dtype=dt))
+        xd = torch.from_numpy(x).to(device="cuda", dtype=tdt)
+        yd = torch.empty_like(xd)
+        for tr in (False, True):
+            yh = ex.apply(x, transpose=tr)
+            ex.apply_device(xd, yd, transpose=tr)
+            torch.cuda.synchronize()
+            assert np.array_equal(yh, yd.double().cpu().numpy()), (dt, tr)
+        if dt == P.DType.f64:
+            assert rel_l2(ex.apply(x), ref) <= TOL64
+        ex.close()
