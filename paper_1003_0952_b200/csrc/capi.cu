@@ -111,7 +111,8 @@ struct csrc_gpu_plan_s {
     int gather_pf = 2;     // L2 prefetch distance in block iterations (0 = off)
     int gather_bpsm = 16;  // resident-grid cap: blocks per SM
     int gather_buf = 0;    // k_gather_buf with U = gather_u (0: k_gather_rows)
-    int gather_u = 8;
+    int gather_u = 4;
+    int gather_nb = 1;     // row-block buffers per block (k_gather_buf)
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
     int gather_grid = 0;
     // host-API pipeline (apply_host): row chunks, and for each the last x chunk it reads
@@ -588,23 +589,23 @@ int grid_for(int device, int64_t work, int per_block);
 // (transpose) value. eval_t only exists for value-unsymmetric matrices.
 template <class T>
 int gather_buf_smem(const Plan& P) {
-    return 16 + 2 * (dev::gather_idx_bytes(P.gather_cap) + dev::gather_val_bytes<T>(P.gather_cap));
+    return 16 + P.gather_nb * (dev::gather_idx_bytes(P.gather_cap) + dev::gather_val_bytes<T>(P.gather_cap));
 }
 
-template <class T, int U>
+template <class T, int U, int NB>
 void* gather_buf_fn_U(int L) {
     switch (L) {
-        case 1: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 1, U>);
-        case 2: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 2, U>);
-        case 8: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 8, U>);
-        case 16: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 16, U>);
-        default: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 4, U>);
+        case 2: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 2, U, NB>);
+        case 8: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 8, U, NB>);
+        case 16: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 16, U, NB>);
+        default: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 4, U, NB>);
     }
 }
 
 template <class T>
-void* gather_buf_fn(int L, int U) {
-    return U == 4 ? gather_buf_fn_U<T, 4>(L) : gather_buf_fn_U<T, 8>(L);
+void* gather_buf_fn(int L, int U, int NB) {
+    if (NB == 1) return U == 4 ? gather_buf_fn_U<T, 4, 1>(L) : gather_buf_fn_U<T, 8, 1>(L);
+    return U == 4 ? gather_buf_fn_U<T, 4, 2>(L) : gather_buf_fn_U<T, 8, 2>(L);
 }
 
 template <class T>
@@ -643,16 +644,34 @@ void setup_gather(Plan& P, const MatView& a) {
     if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
 
     const double avg = n ? static_cast<double>(ne) / n : 0.0;
-    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 10 ? 2 : avg <= 128 ? 4 : 8);
+    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? 2 : avg <= 128 ? 4 : 8);
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
     P.gather_bpsm = env_int("CSRC_GPU_GBPSM", 16);  // 256-thread blocks per SM
     {
-        // host pipeline: C row chunks on multiples of 256 rows (any lane count's block)
-        const int64_t want = std::max<int64_t>(1, std::min<int64_t>(env_int("CSRC_GPU_HOST_CHUNKS", 16), n / (1 << 18)));
-        const int64_t step = ((n + want - 1) / want + 255) / 256 * 256;
+        // host pipeline: row chunks on multiples of 256 rows (any lane count's block).
+        // Ramped sizes (in 64ths of n): a small first chunk starts the y download
+        // early, small last chunks shorten the compute + download tail after the
+        // last x chunk lands. CSRC_GPU_HOST_CHUNKS=c forces c equal chunks.
         P.hchunk.clear();
-        for (int64_t r = 0; r < n; r += step) P.hchunk.push_back(static_cast<int32_t>(r));
-        P.hchunk.push_back(n);
+        const int forced = env_int("CSRC_GPU_HOST_CHUNKS", 0);
+        std::vector<int> units;
+        if (forced > 0)
+            units.assign(forced, 1);
+        else if (n >= (int64_t(1) << 20))
+            units = {2, 4, 8, 8, 8, 8, 8, 8, 4, 2, 2, 1, 1};
+        else
+            units = {1};
+        int64_t tot = 0;
+        for (int u : units) tot += u;
+        int64_t acc = 0;
+        P.hchunk.push_back(0);
+        for (int u : units) {
+            acc += u;
+            int64_t b = (n * acc / tot + 255) / 256 * 256;
+            b = std::min<int64_t>(b, n);
+            if (b > P.hchunk.back()) P.hchunk.push_back(static_cast<int32_t>(b));
+        }
+        if (P.hchunk.back() != n) P.hchunk.push_back(n);
         const int nc = static_cast<int>(P.hchunk.size()) - 1;
         P.hneed.assign(nc, 0);
         for (int c = 0; c < nc; ++c) {
@@ -664,15 +683,16 @@ void setup_gather(Plan& P, const MatView& a) {
         }
     }
     // double-buffered form: needs the largest row-block span to fit twice in shared memory
-    P.gather_u = env_int("CSRC_GPU_GU", 8) == 4 ? 4 : 8;
+    P.gather_u = env_int("CSRC_GPU_GU", 4) == 8 ? 8 : 4;
+    P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
     if (env_int("CSRC_GPU_GBUF", 1) != 0) {
         const int R = 256 / P.gather_lanes;
         int64_t cap = 0;
         for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
-        const int64_t bytes = 16 + 2 * (((cap + 8) * 4 + 15) / 16 * 16 + ((cap + 8) * static_cast<int64_t>(sizeof(T)) + 15) / 16 * 16);
+        const int64_t bytes = 16 + P.gather_nb * (((cap + 8) * 4 + 15) / 16 * 16 + ((cap + 8) * static_cast<int64_t>(sizeof(T)) + 15) / 16 * 16);
         if (bytes <= 100 * 1024) {
             P.gather_cap = static_cast<int>(cap);
-            void* fn = gather_buf_fn<T>(P.gather_lanes, P.gather_u);
+            void* fn = gather_buf_fn<T>(P.gather_lanes, P.gather_u, P.gather_nb);
             const int smem = gather_buf_smem<T>(P);
             CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             int occ = 0;
@@ -729,7 +749,7 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
         const int64_t blocks = (static_cast<int64_t>(r1 - r0) + R - 1) / R;
         const int grid = static_cast<int>(std::min<int64_t>(blocks, P.gather_grid));
         void* args[] = {&A};
-        CUDA_OK(cudaLaunchKernel(gather_buf_fn<T>(P.gather_lanes, P.gather_u), dim3(grid), dim3(256),
+        CUDA_OK(cudaLaunchKernel(gather_buf_fn<T>(P.gather_lanes, P.gather_u, P.gather_nb), dim3(grid), dim3(256),
                                  args, static_cast<size_t>(gather_buf_smem<T>(P)), st));
         return;
     }
@@ -1104,12 +1124,21 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
     double* xd64 = f32 ? P.dxd.as<double>() : P.dx.as<double>();
     double* yd64 = f32 ? P.dyd.as<double>() : P.dy.as<double>();
     cudaStream_t st = P.stream;
+    // CSRC_GPU_HOST_TRACE=1: per-chunk timeline on stderr (diagnostics only)
+    const bool trace = env_int("CSRC_GPU_HOST_TRACE", 0) != 0;
+    std::vector<cudaEvent_t> tr_ev;
+    if (trace) {
+        tr_ev.resize(1 + 3 * nc);
+        for (auto& e : tr_ev) CUDA_OK(cudaEventCreate(&e));
+        CUDA_OK(cudaEventRecord(tr_ev[0], st));
+    }
     CUDA_OK(cudaEventRecord(P.ev_in, st));
     CUDA_OK(cudaStreamWaitEvent(P.s_h2d, P.ev_in, 0));  // after earlier work on the plan stream
     for (int c = 0; c < nc; ++c) {
         const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
         CUDA_OK(cudaMemcpyAsync(xd64 + r0, xh + r0, len * 8, cudaMemcpyHostToDevice, P.s_h2d));
         CUDA_OK(cudaEventRecord(P.ev_x[c], P.s_h2d));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + c], P.s_h2d));
     }
     int have = -1;  // x chunks the compute stream already waited for (and converted)
     for (int c = 0; c < nc; ++c) {
@@ -1131,12 +1160,26 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         }
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaEventRecord(P.ev_y[c], st));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + nc + c], st));
         CUDA_OK(cudaStreamWaitEvent(P.s_d2h, P.ev_y[c], 0));
         CUDA_OK(cudaMemcpyAsync(yh + r0, yd64 + r0, static_cast<size_t>(r1 - r0) * 8,
                                 cudaMemcpyDeviceToHost, P.s_d2h));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + 2 * nc + c], P.s_d2h));
     }
     CUDA_OK(cudaStreamSynchronize(P.s_d2h));
     CUDA_OK(cudaStreamSynchronize(st));
+    if (trace) {
+        std::fprintf(stderr, "host pipeline: %d chunks (ms from start: x landed / rows done / y landed)\n", nc);
+        for (int c = 0; c < nc; ++c) {
+            float a = 0, b = 0, d = 0;
+            cudaEventElapsedTime(&a, tr_ev[0], tr_ev[1 + c]);
+            cudaEventElapsedTime(&b, tr_ev[0], tr_ev[1 + nc + c]);
+            cudaEventElapsedTime(&d, tr_ev[0], tr_ev[1 + 2 * nc + c]);
+            std::fprintf(stderr, "  chunk %2d rows %9d..%9d need x<=%2d : %7.3f %7.3f %7.3f\n", c,
+                         P.hchunk[c], P.hchunk[c + 1], P.hneed[c], a, b, d);
+        }
+        for (auto e : tr_ev) cudaEventDestroy(e);
+    }
 }
 
 void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {

@@ -93,10 +93,12 @@ __global__ void __launch_bounds__(256) k_gather_rows(const int32_t* __restrict__
     }
 }
 
-// Double-buffered form: each 256-thread block walks row blocks of R = 256 / L
-// rows; thread 0 stages the NEXT row block's eidx / eval spans into shared
-// memory with two cp.async.bulk copies (mbarrier completion) while the block
-// computes the current one. A lane then issues all U gathers of x for its
+// Staged form: each 256-thread block walks row blocks of R = 256 / L rows;
+// thread 0 stages a row block's eidx / eval spans into shared memory with two
+// cp.async.bulk copies (mbarrier completion). NB = 2: the next row block is
+// copied while the block computes the current one; NB = 1: half the shared
+// memory, more resident blocks, the copy latency hidden by the other blocks
+// on the SM. A lane then issues all U gathers of x for its
 // entries back to back from shared-memory indices, so a row costs one global
 // round trip instead of one per entry pair. cap = largest entry span of any
 // row block (plan time).
@@ -121,8 +123,9 @@ struct GBufArgs {
     int32_t val_bytes;  // per buffer, 16-aligned, >= sizeof(T) * (cap + 8)
 };
 
-template <typename T, int L, int U>
+template <typename T, int L, int U, int NB>
 __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
+    static_assert(NB == 1 || NB == 2, "one or two row-block buffers");
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int R = 256 / L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2]
@@ -164,8 +167,8 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
     constexpr int kValAlign = 16 / sizeof(T);
     int it = 0;
     for (int64_t base = first; base < A.nrows; base += stride, ++it) {
-        const int buf = it & 1;
-        if (threadIdx.x == 0 && base + stride < A.nrows) {
+        const int buf = NB == 2 ? (it & 1) : 0;
+        if (NB == 2 && threadIdx.x == 0 && base + stride < A.nrows) {
             issue(buf ^ 1, nx0, nx1);  // buffer buf^1 was released by the last __syncthreads
             span(base + 2 * stride, nx0, nx1);
         }
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
             xr = __ldg(A.x + row);
         }
         const int32_t e_base = __ldg(A.eptr + base);  // the block's first entry
-        mbar_wait(&full[buf], (it >> 1) & 1);
+        mbar_wait(&full[buf], NB == 2 ? ((it >> 1) & 1) : (it & 1));
         const uint32_t st = smem_u32(bufs + buf * buf_bytes);
         const uint32_t ib = st - 4u * static_cast<uint32_t>(e_base & ~(kIdxAlign - 1));
         const uint32_t vb = st + A.idx_bytes -
@@ -210,6 +213,10 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
         for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
         if (act && sub == 0) A.y[row] = s + d * xr;
         __syncthreads();
+        if (NB == 1 && threadIdx.x == 0 && base + stride < A.nrows) {
+            issue(0, nx0, nx1);  // single buffer: refill once every thread is done with it
+            span(base + 2 * stride, nx0, nx1);
+        }
     }
 }
 
