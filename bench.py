@@ -339,7 +339,8 @@ def main():
         gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
         roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                       traffic=load_traffic(wl), peak_source=peak_src,
-                      kernel=f"k_{args.kind}" if args.kind in ("gather", "windowed", "atomic") else args.kind,
+                      kernel={"gather": "k_gather_buf", "windowed": "k_windowed", "atomic": "k_atomic"}.get(
+                          args.kind, args.kind),
                       algorithmic_bytes_per_launch=mb, kernel_ms=kms),
         e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
                  else (p.row_end - p.lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1

@@ -63,15 +63,16 @@ typedef struct {
 
 /* Strategy kinds. SEQUENTIAL / LOCAL_BUFFERS / COLORFUL mirror
  * csrc::StrategyKind (parallel.hpp:16); ATOMIC and WINDOWED are the GPU-only
- * kernels the north star asks for. */
+ * kernels the north star asks for; GATHER is the fastest. */
 enum {
-    CSRC_KIND_SEQUENTIAL = 0,   /* one-CTA-free path: the windowed kernel, no buffers */
+    CSRC_KIND_SEQUENTIAL = 0,   /* no buffers: the gather kernel (windowed for band plans) */
     CSRC_KIND_LOCAL_BUFFERS = 1,/* windowed kernel into private band buffers + accumulation pass */
     CSRC_KIND_COLORFUL = 2,     /* one launch per conflict-free row class, no atomics */
     CSRC_KIND_ATOMIC = 3,       /* global fp64/fp32 red.global scatter baseline */
     CSRC_KIND_WINDOWED = 4,     /* TMA tiles, smem y rings, red.global flush (CSRC model bytes) */
-    CSRC_KIND_GATHER = 5        /* transposed gather: plan adds the CSR index of the upper
-                                   triangle (+4 B/pair over the CSRC model), no scatter at all */
+    CSRC_KIND_GATHER = 5        /* transposed gather: the plan lays out each row's lower pairs and
+                                   the pairs naming it as column as one entry stream (+4 B/pair
+                                   over the CSRC model), no scatter, bit-reproducible */
 };
 
 /* csrc::AccumMethod (parallel.hpp:17) */

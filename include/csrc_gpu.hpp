@@ -69,6 +69,7 @@ struct Strategy {
 
     static Strategy windowed() { return Strategy(CSRC_KIND_WINDOWED, CSRC_ACCUM_EFFECTIVE, 1); }
     static Strategy atomic() { return Strategy(CSRC_KIND_ATOMIC, CSRC_ACCUM_EFFECTIVE, 1); }
+    static Strategy gather() { return Strategy(CSRC_KIND_GATHER, CSRC_ACCUM_EFFECTIVE, 1); }
 
     csrc_gpu_strategy c() const {
         return csrc_gpu_strategy{kind, accum, p, dtype, conflict_mode, color_order, device, bands};
