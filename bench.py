@@ -211,7 +211,7 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--kind", default="gather", choices=["gather", "windowed", "atomic", "colorful", "local_buffers"])
-    ap.add_argument("--compare", default="windowed,atomic",
+    ap.add_argument("--compare", default="gather_explicit,windowed,atomic",
                     help="other kernels timed on the same workload (reported under 'kernels'); '' = none")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
@@ -252,12 +252,19 @@ def main():
         ms = float(np.mean(tot))
         kms = float(np.mean(ker))
         info = ex.info()
+        layout_bytes, row_patterns = int(info.stream_bytes), int(info.row_patterns)
         # our kernels per product (the y memset of windowed/atomic is a driver memset, not counted)
         launches_per_step = 1 if args.kind in ("gather", "windowed", "atomic") else info.launches_per_apply
         others = {}
         for name in [k for k in args.compare.split(",") if k and k != args.kind]:
-            ox = P.GpuSpmv(a, P.Strategy(P.StrategyKind[name], P.AccumMethod.interval, p=8, dtype=dtype,
-                                          device=local))
+            # gather_explicit: the gather kernel with explicit column indices (row-pattern form off)
+            env_off = name == "gather_explicit"
+            if env_off:
+                os.environ["CSRC_GPU_GPATTERN"] = "0"
+            ox = P.GpuSpmv(a, P.Strategy(P.StrategyKind["gather" if env_off else name], P.AccumMethod.interval,
+                                          p=8, dtype=dtype, device=local))
+            if env_off:
+                del os.environ["CSRC_GPU_GPATTERN"]
             for _ in range(3):
                 ox.apply_device(xd, yd)
             otot, oker = ox.time_products(xd, yd, min(args.steps, 50), flush)
@@ -277,6 +284,7 @@ def main():
         ms_max = ms
     else:
         others = {}
+        layout_bytes, row_patterns = None, 0
         from paper_1003_0952_b200.dist import DistSpmv
         ds = DistSpmv(a, strat)
         p = ds.plan
@@ -339,9 +347,12 @@ def main():
         gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
         roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                       traffic=load_traffic(wl), peak_source=peak_src,
-                      kernel={"gather": "k_gather_buf", "windowed": "k_windowed", "atomic": "k_atomic"}.get(
+                      kernel={"gather": "k_gather_staged", "windowed": "k_windowed", "atomic": "k_atomic"}.get(
                           args.kind, args.kind),
-                      algorithmic_bytes_per_launch=mb, kernel_ms=kms),
+                      algorithmic_bytes_per_launch=mb, kernel_ms=kms,
+                      layout_bytes_per_launch=layout_bytes,
+                      layout_frac=(layout_bytes / (kms / 1e3) / 1e9) / peak if layout_bytes else None,
+                      row_patterns=row_patterns),
         e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
                  else (p.row_end - p.lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
                  else (p.row_end - p.row_begin) * 8, wall_ms_per_step=e2e_s * 1e3),

@@ -126,11 +126,15 @@ typedef struct {
     int64_t device_bytes;       /* device memory held by the plan                 */
     int32_t n_windows;          /* windowed: scatter-distance windows             */
     int32_t win_lo[6], win_hi[6]; /* windowed: distance interval of each window   */
-    int32_t lanes;              /* windowed: lanes per row                        */
-    int32_t stages;             /* windowed: TMA pipeline depth                   */
-    int32_t smem_bytes;         /* windowed: dynamic shared memory per CTA        */
+    int32_t lanes;              /* windowed / gather: lanes per row               */
+    int32_t stages;             /* windowed: TMA pipeline depth; gather: buffers  */
+    int32_t smem_bytes;         /* windowed / gather: dynamic shared memory per CTA */
     int32_t launches_per_apply; /* kernels launched per product                   */
     double  captured_fraction;  /* windowed: pairs whose scatter lands in a window */
+    int64_t stream_bytes;       /* bytes one product moves in the plan's device layout
+                                   (= model_bytes for the CSRC kernels; gather: its entry
+                                   stream)                          */
+    int32_t row_patterns;       /* gather: column-offset patterns (0 = explicit indices) */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;

@@ -80,6 +80,8 @@ class PlanInfo(C.Structure):
         ("smem_bytes", i32),
         ("launches_per_apply", i32),
         ("captured_fraction", f64),
+        ("stream_bytes", i64),
+        ("row_patterns", i32),
     ]
 
 

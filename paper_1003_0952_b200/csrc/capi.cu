@@ -5,6 +5,7 @@
 // windows, colour classes, private buffers) and a stream; apply() enqueues
 // init / compute / accumulate phases and records PhaseTimings-style events.
 #include <algorithm>
+#include <unordered_map>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -113,6 +114,11 @@ struct csrc_gpu_plan_s {
     int gather_buf = 0;    // k_gather_buf with U = gather_u (0: k_gather_rows)
     int gather_u = 4;
     int gather_nb = 1;     // row-block buffers per block (k_gather_buf)
+    // row-pattern form (k_gather_pat): pattern id per row, offset table
+    int gather_pat = 0;
+    int gather_nt = 256;   // threads per block (k_gather_staged)
+    int32_t n_patterns = 0;
+    DevBuf pbase, pat_off;
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
     int gather_grid = 0;
     // host-API pipeline (apply_host): row chunks, and for each the last x chunk it reads
@@ -587,25 +593,72 @@ int grid_for(int device, int64_t work, int per_block);
 // Entry stream per row q: lower pairs of q (ja / al, CSRC order), then the
 // pairs (r, q), r > q ascending, with their au (normal product) or al
 // (transpose) value. eval_t only exists for value-unsymmetric matrices.
-template <class T>
-int gather_buf_smem(const Plan& P) {
-    return 16 + P.gather_nb * (dev::gather_idx_bytes(P.gather_cap) + dev::gather_val_bytes<T>(P.gather_cap));
-}
-
-template <class T, int U, int NB>
-void* gather_buf_fn_U(int L) {
-    switch (L) {
-        case 2: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 2, U, NB>);
-        case 8: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 8, U, NB>);
-        case 16: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 16, U, NB>);
-        default: return reinterpret_cast<void*>(&dev::k_gather_buf<T, 4, U, NB>);
+// Dictionary of per-row column-offset patterns (offsets c - q in entry
+// order); pbase[q] = start of row q's pattern in pat_off. Gives up (returns
+// false) past 65535 patterns or 1 M stored offsets: then the plan keeps
+// explicit column indices.
+bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const std::vector<int32_t>& eidx,
+                       std::vector<int32_t>& pbase, std::vector<int32_t>& pat_off, int32_t* n_patterns) {
+    pbase.assign(static_cast<size_t>(n), 0);
+    pat_off.clear();
+    std::vector<int32_t> pat_ptr(1, 0);
+    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+    for (index_t q = 0; q < n; ++q) {
+        const int32_t e0 = eptr[q], len = eptr[q + 1] - e0;
+        uint64_t h = 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(len);
+        for (int32_t j = 0; j < len; ++j)
+            h = (h ^ static_cast<uint32_t>(eidx[e0 + j] - q)) * 0x100000001B3ull;
+        auto& cand = by_hash[h];
+        int32_t found = -1;
+        for (int32_t p : cand) {
+            const int32_t p0 = pat_ptr[p];
+            if (pat_ptr[p + 1] - p0 != len) continue;
+            bool same = true;
+            for (int32_t j = 0; j < len && same; ++j) same = pat_off[p0 + j] == eidx[e0 + j] - q;
+            if (same) {
+                found = p;
+                break;
+            }
+        }
+        if (found < 0) {
+            found = static_cast<int32_t>(pat_ptr.size()) - 1;
+            if (found >= 65535 || pat_off.size() + len > (size_t(1) << 20)) return false;
+            for (int32_t j = 0; j < len; ++j) pat_off.push_back(eidx[e0 + j] - q);
+            pat_ptr.push_back(static_cast<int32_t>(pat_off.size()));
+            cand.push_back(found);
+        }
+        pbase[q] = pat_ptr[found];
     }
+    *n_patterns = static_cast<int32_t>(pat_ptr.size()) - 1;
+    if (pat_off.empty()) pat_off.push_back(0);  // keep the device table non-empty
+    return true;
 }
 
 template <class T>
-void* gather_buf_fn(int L, int U, int NB) {
-    if (NB == 1) return U == 4 ? gather_buf_fn_U<T, 4, 1>(L) : gather_buf_fn_U<T, 8, 1>(L);
-    return U == 4 ? gather_buf_fn_U<T, 4, 2>(L) : gather_buf_fn_U<T, 8, 2>(L);
+int gather_stage_smem(const Plan& P) {
+    return 16 + P.gather_nb * ((P.gather_pat ? 0 : dev::gather_idx_bytes(P.gather_cap)) +
+                               dev::gather_val_bytes<T>(P.gather_cap));
+}
+
+template <class T, int L, int U, int NB>
+void* gather_stage_fn_NB(bool pat) {
+    return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true>)
+               : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false>);
+}
+
+template <class T, int L>
+void* gather_stage_fn_L(int U, int NB, bool pat) {
+    if (U == 8) return NB == 2 ? gather_stage_fn_NB<T, L, 8, 2>(pat) : gather_stage_fn_NB<T, L, 8, 1>(pat);
+    return NB == 2 ? gather_stage_fn_NB<T, L, 4, 2>(pat) : gather_stage_fn_NB<T, L, 4, 1>(pat);
+}
+
+template <class T>
+void* gather_stage_fn(const Plan& P) {
+    switch (P.gather_lanes) {
+        case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, P.gather_pat);
+        case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, P.gather_pat);
+        default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, P.gather_pat);
+    }
 }
 
 template <class T>
@@ -639,7 +692,6 @@ void setup_gather(Plan& P, const MatView& a) {
             if (!a.value_symmetric) evt[w] = a.al[t];
         }
     upload(P.eptr, eptr.data(), eptr.size());
-    upload(P.eidx, eidx.data(), eidx.size());
     upload_values<T>(P.eval, ev.data(), ev.size());
     if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
 
@@ -682,27 +734,43 @@ void setup_gather(Plan& P, const MatView& a) {
                                               P.hchunk.begin()) - 1;
         }
     }
-    // double-buffered form: needs the largest row-block span to fit twice in shared memory
-    P.gather_u = env_int("CSRC_GPU_GU", 4) == 8 ? 8 : 4;
+    // staged form (k_gather_staged): U x-gathers in flight per lane, NB buffers,
+    // NT threads per block; the row-pattern form when the rows repeat a small
+    // dictionary of column-offset patterns
+    P.gather_u = env_int("CSRC_GPU_GU", avg / P.gather_lanes <= 16 ? 8 : 4) == 8 ? 8 : 4;
     P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
-    if (env_int("CSRC_GPU_GBUF", 1) != 0) {
-        const int R = 256 / P.gather_lanes;
+    P.gather_nt = env_int("CSRC_GPU_GNT", 256) == 128 ? 128 : 256;
+    std::vector<int32_t> pbase, pat_off;
+    if (env_int("CSRC_GPU_GPATTERN", 1) != 0 && P.gather_lanes <= 8)
+        P.gather_pat = find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns) ? 1 : 0;
+    if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 2 && P.gather_lanes <= 8) {
+        const int R = P.gather_nt / P.gather_lanes;
         int64_t cap = 0;
         for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
-        const int64_t bytes = 16 + P.gather_nb * (((cap + 8) * 4 + 15) / 16 * 16 + ((cap + 8) * static_cast<int64_t>(sizeof(T)) + 15) / 16 * 16);
-        if (bytes <= 100 * 1024) {
+        if (cap <= 16384) {
             P.gather_cap = static_cast<int>(cap);
-            void* fn = gather_buf_fn<T>(P.gather_lanes, P.gather_u, P.gather_nb);
-            const int smem = gather_buf_smem<T>(P);
-            CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            int occ = 0;
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
-            if (occ >= 1) {
-                P.gather_buf = 1;
-                const int64_t blocks = (n + R - 1) / R;
-                P.gather_grid = static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(num_sms(P.device)) * occ));
+            const int smem = gather_stage_smem<T>(P);
+            if (smem <= 100 * 1024) {
+                void* fn = gather_stage_fn<T>(P);
+                CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                int occ = 0;
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P.gather_nt, smem));
+                if (occ >= 1) {
+                    P.gather_buf = 1;
+                    const int64_t blocks = (n + R - 1) / R;
+                    P.gather_grid = static_cast<int>(
+                        std::min<int64_t>(blocks, static_cast<int64_t>(num_sms(P.device)) * occ));
+                }
             }
         }
+    }
+    if (!P.gather_buf) P.gather_pat = 0;  // the plain row kernel reads explicit indices
+    if (P.gather_pat) {
+        upload(P.pbase, pbase.data(), pbase.size());
+        upload(P.pat_off, pat_off.data(), pat_off.size());
+    } else {
+        P.n_patterns = 0;
+        upload(P.eidx, eidx.data(), eidx.size());
     }
 }
 
@@ -734,23 +802,25 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
     if (r1 <= r0) return;
     const T* vals = (tr && !P.value_symmetric ? P.eval_t : P.eval).template as<T>();
     if (P.gather_buf) {
-        const int R = 256 / P.gather_lanes;
-        dev::GBufArgs<T> A;
+        const int R = P.gather_nt / P.gather_lanes;
+        dev::GStageArgs<T> A;
         A.eptr = P.eptr.as<int32_t>();
         A.eidx = P.eidx.as<int32_t>();
+        A.pbase = P.pbase.as<int32_t>();
+        A.pat_off = P.pat_off.as<int32_t>();
         A.eval = vals;
         A.ad = P.ad.as<T>();
         A.x = x;
         A.y = y;
         A.row0 = r0;
         A.nrows = r1;
-        A.idx_bytes = dev::gather_idx_bytes(P.gather_cap);
+        A.idx_bytes = P.gather_pat ? 0 : dev::gather_idx_bytes(P.gather_cap);
         A.val_bytes = dev::gather_val_bytes<T>(P.gather_cap);
         const int64_t blocks = (static_cast<int64_t>(r1 - r0) + R - 1) / R;
         const int grid = static_cast<int>(std::min<int64_t>(blocks, P.gather_grid));
         void* args[] = {&A};
-        CUDA_OK(cudaLaunchKernel(gather_buf_fn<T>(P.gather_lanes, P.gather_u, P.gather_nb), dim3(grid), dim3(256),
-                                 args, static_cast<size_t>(gather_buf_smem<T>(P)), st));
+        CUDA_OK(cudaLaunchKernel(gather_stage_fn<T>(P), dim3(grid), dim3(P.gather_nt), args,
+                                 static_cast<size_t>(gather_stage_smem<T>(P)), st));
         return;
     }
     switch (P.gather_lanes) {
@@ -1311,7 +1381,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.dx, &P.dy, &P.dxd, &P.dyd})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS
@@ -1325,6 +1395,21 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         info->smem_bytes = static_cast<int32_t>(P.win_smem);
         info->launches_per_apply = P.launches;
         info->captured_fraction = P.captured;
+        info->stream_bytes = info->model_bytes;
+        info->row_patterns = 0;
+        if (P.exec_kind == CSRC_KIND_GATHER) {
+            const int64_t ne = P.nrows ? static_cast<int64_t>(2) * P.k : 0;
+            const int64_t vs = static_cast<int64_t>(P.vsize());
+            // entry values + (indices | per-row pattern start) + eptr + ad, x, y
+            info->stream_bytes = ne * vs + (P.gather_pat ? 4 * static_cast<int64_t>(P.nrows) : 4 * ne) +
+                                 4 * (static_cast<int64_t>(P.nrows) + 1) + 3 * vs * P.nrows;
+            info->row_patterns = P.gather_pat ? P.n_patterns : 0;
+            info->lanes = P.gather_lanes;
+            info->stages = P.gather_buf ? P.gather_nb : 0;
+            info->smem_bytes = P.gather_buf ? (P.dtype == CSRC_DTYPE_F64 ? gather_stage_smem<double>(P)
+                                                                         : gather_stage_smem<float>(P))
+                                            : 0;
+        }
     });
 }
 

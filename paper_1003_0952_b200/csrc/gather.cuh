@@ -93,15 +93,39 @@ __global__ void __launch_bounds__(256) k_gather_rows(const int32_t* __restrict__
     }
 }
 
-// Staged form: each 256-thread block walks row blocks of R = 256 / L rows;
-// thread 0 stages a row block's eidx / eval spans into shared memory with two
-// cp.async.bulk copies (mbarrier completion). NB = 2: the next row block is
-// copied while the block computes the current one; NB = 1: half the shared
-// memory, more resident blocks, the copy latency hidden by the other blocks
-// on the SM. A lane then issues all U gathers of x for its
-// entries back to back from shared-memory indices, so a row costs one global
-// round trip instead of one per entry pair. cap = largest entry span of any
-// row block (plan time).
+// Staged form (k_gather_staged): each block walks row blocks of
+// R = blockDim.x / L rows (grid-stride); thread 0 stages a row block's spans
+// into shared memory with cp.async.bulk copies completing on an mbarrier.
+// A lane then issues all U gathers of x for its next U entries back to back,
+// so a row costs one global round trip per U entries instead of one per entry.
+//   NB = 2: the next row block is copied while the block computes this one;
+//   NB = 1: half the shared memory -> more resident blocks, the copy latency
+//           hidden by the other blocks on the SM.
+//   PAT = false: eidx and eval spans are staged, column = eidx[e];
+//   PAT = true : row-pattern form. Mesh matrices repeat a handful of
+//           column-offset patterns (27-point stencil: 27, interior plus
+//           boundary cases); the plan stores per row the start of its pattern
+//           in a small offset table (pbase, int32) instead of a 4-byte column
+//           index per entry: column = row + pat_off[pbase[row] + j]. Only the
+//           value span is staged; the table (a few KB) stays in L1.
+// The per-row entry order is the same in every form, so for equal L and U
+// the results are bit-identical.
+template <typename T>
+struct GStageArgs {
+    const int32_t* eptr;
+    const int32_t* eidx;     // !PAT
+    const int32_t* pbase;    // PAT: pattern start per row
+    const int32_t* pat_off;  // PAT
+    const T* eval;
+    const T* ad;
+    const T* x;
+    T* y;
+    int32_t row0;       // rows [row0, nrows); row0 a multiple of R
+    int32_t nrows;
+    int32_t idx_bytes;  // per buffer, 16-aligned (0 when PAT)
+    int32_t val_bytes;  // per buffer, 16-aligned
+};
+
 // shared-memory bytes of one buffer holding up to `cap` entries (+ alignment slack)
 __host__ __device__ inline int gather_idx_bytes(int cap) { return ((cap + 8) * 4 + 15) & ~15; }
 template <typename T>
@@ -109,25 +133,11 @@ __host__ __device__ inline int gather_val_bytes(int cap) {
     return ((cap + 8) * static_cast<int>(sizeof(T)) + 15) & ~15;
 }
 
-template <typename T>
-struct GBufArgs {
-    const int32_t* eptr;
-    const int32_t* eidx;
-    const T* eval;
-    const T* ad;
-    const T* x;
-    T* y;
-    int32_t row0;       // rows [row0, nrows); row0 a multiple of R
-    int32_t nrows;
-    int32_t idx_bytes;  // per buffer, 16-aligned, >= 4 * (cap + 8)
-    int32_t val_bytes;  // per buffer, 16-aligned, >= sizeof(T) * (cap + 8)
-};
-
-template <typename T, int L, int U, int NB>
-__global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
+template <typename T, int L, int U, int NB, bool PAT>
+__global__ void __launch_bounds__(256) k_gather_staged(const GStageArgs<T> A) {
     static_assert(NB == 1 || NB == 2, "one or two row-block buffers");
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int R = 256 / L;
+    const int R = blockDim.x / L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2]
     unsigned char* bufs = smem + 16;
     const int buf_bytes = A.idx_bytes + A.val_bytes;
@@ -135,7 +145,7 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
     const int rrel = threadIdx.x / L;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * R;
     const int64_t first = A.row0 + static_cast<int64_t>(blockIdx.x) * R;
-    // thread 0: entry span of the row block two iterations ahead (register pipeline)
+    // thread 0: entry span of the next row block to stage (register pipeline)
     int32_t nx0 = 0, nx1 = 0;
     auto span = [&](int64_t b, int32_t& e0, int32_t& e1) {
         if (b < A.nrows) {
@@ -144,11 +154,15 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
         }
     };
     auto issue = [&](int buf, int32_t e0, int32_t e1) {
-        const Seg<int32_t> si = seg(A.eidx, e0, e1);
-        const Seg<T> sv = seg(A.eval, e0, e1);
         unsigned char* st = bufs + buf * buf_bytes;
-        mbar_expect_tx(&full[buf], si.bytes + sv.bytes);
-        tma_load(st, si.src, si.bytes, &full[buf]);
+        const Seg<T> sv = seg(A.eval, e0, e1);
+        if (PAT) {
+            mbar_expect_tx(&full[buf], sv.bytes);
+        } else {
+            const Seg<int32_t> si = seg(A.eidx, e0, e1);
+            mbar_expect_tx(&full[buf], si.bytes + sv.bytes);
+            tma_load(st, si.src, si.bytes, &full[buf]);
+        }
         tma_load(st + A.idx_bytes, sv.src, sv.bytes, &full[buf]);
     };
     if (threadIdx.x == 0) {
@@ -174,20 +188,22 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
         }
         const int64_t row = base + rrel;
         const bool act = row < A.nrows;
-        int32_t eb = 0, ee = 0;
+        int32_t eb = 0, ee = 0, pb = 0;
         T d = T(0), xr = T(0);
         if (act) {
             eb = __ldg(A.eptr + row);
             ee = __ldg(A.eptr + row + 1);
+            if (PAT) pb = __ldg(A.pbase + row) - eb;  // pattern slot of entry f = pb + f
             d = __ldg(A.ad + row);
             xr = __ldg(A.x + row);
         }
-        const int32_t e_base = __ldg(A.eptr + base);  // the block's first entry
+        const int32_t e_base = __ldg(A.eptr + base);  // the row block's first entry
         mbar_wait(&full[buf], NB == 2 ? ((it >> 1) & 1) : (it & 1));
         const uint32_t st = smem_u32(bufs + buf * buf_bytes);
         const uint32_t ib = st - 4u * static_cast<uint32_t>(e_base & ~(kIdxAlign - 1));
         const uint32_t vb = st + A.idx_bytes -
                             static_cast<uint32_t>(sizeof(T)) * static_cast<uint32_t>(e_base & ~(kValAlign - 1));
+        const T* xrow = A.x + row;
         T acc0 = T(0), acc1 = T(0);
         for (int32_t e = eb + sub; e < ee; e += U * L) {
             T xv[U];
@@ -195,7 +211,7 @@ __global__ void __launch_bounds__(256) k_gather_buf(const GBufArgs<T> A) {
             for (int u = 0; u < U; ++u) {
                 const int32_t f = e + u * L;
                 xv[u] = T(0);
-                if (f < ee) xv[u] = __ldg(A.x + lds_i(ib + 4u * f));
+                if (f < ee) xv[u] = PAT ? __ldg(xrow + __ldg(A.pat_off + pb + f)) : __ldg(A.x + lds_i(ib + 4u * f));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {

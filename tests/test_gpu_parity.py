@@ -325,3 +325,90 @@ def test_host_pipeline_matches_device(cfg):
         if dt == P.DType.f64:
             assert rel_l2(ex.apply(x), ref) <= TOL64
         ex.close()
+
+
+GATHER_SHAPES = [
+    {"CSRC_GPU_GPATTERN": "0"},
+    {"CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GLANES": "4"},
+    {"CSRC_GPU_GLANES": "8", "CSRC_GPU_GU": "8"},
+    {"CSRC_GPU_GBUF": "0", "CSRC_GPU_GLANES": "1"},
+    {"CSRC_GPU_GBUF": "0", "CSRC_GPU_GLANES": "4", "CSRC_GPU_GPF": "2"},
+    {"CSRC_GPU_GBUF": "0", "CSRC_GPU_GLANES": "16"},
+    {"CSRC_GPU_GNB": "2", "CSRC_GPU_GLANES": "2", "CSRC_GPU_GU": "8"},
+    {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "8", "CSRC_GPU_GU": "4"},
+    {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "16", "CSRC_GPU_GU": "8"},
+]
+
+
+@pytest.mark.parametrize("shape", range(len(GATHER_SHAPES)))
+def test_gather_kernel_shapes(shape, monkeypatch):
+    """Every gather kernel shape the plan can select (plain / staged, lanes,
+    unroll, buffers; read from the environment at plan creation) gives the
+    same bits as the default shape: the per-row summation order depends only
+    on the lane count, so results are compared against the oracle and, for
+    equal lane counts, bit for bit."""
+    for k, v in GATHER_SHAPES[shape].items():
+        monkeypatch.setenv(k, v)
+    for idx in (0, 3, 5):
+        p = f"g{idx}_"
+        a = MESH.matrix(p)
+        y = run(a, MESH[p + "x"], P.Strategy(K.gather))
+        assert rel_l2(y, MESH[p + "y"]) <= TOL64
+        yt = run(a, MESH[p + "x"], P.Strategy(K.gather), transpose=True)
+        assert rel_l2(yt, O.spmv_csrc(a, MESH[p + "x"], transpose=True)) <= TOL64
+    for idx in range(0, 29, 4):
+        p = f"m{idx}_"
+        a = FAM.matrix(p)
+        assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.gather)), FAM[p + "y"]) <= TOL64
+
+
+def test_gather_dense_row_falls_back():
+    """An arrow matrix whose first column is full: row 0's entry stream (every
+    other row names it) does not fit a shared-memory row block, so the plan
+    takes the plain row kernel; results still match the oracle."""
+    n = 40000
+    rng = np.random.default_rng(5)
+    ia = np.zeros(n + 1, np.int32)
+    ia[1:] = np.arange(n, dtype=np.int32)  # row r >= 1 stores the single pair (r, 0)
+    ja = np.zeros(n - 1, np.int32)
+    al = rng.uniform(-1, 1, n - 1)
+    au = rng.uniform(-1, 1, n - 1)
+    ad = 4 + rng.uniform(0, 1, n)
+    a = P.CsrcMatrix(n, ad, ia, ja, al, au)
+    x = rng.uniform(-1, 1, n)
+    for kind in (K.gather, K.sequential):
+        y = run(a, x, P.Strategy(kind))
+        assert rel_l2(y, O.spmv_csrc(a, x)) <= TOL64
+        assert rel_l2(run(a, x, P.Strategy(kind), transpose=True), O.spmv_csrc(a, x, transpose=True)) <= TOL64
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+def test_row_patterns_are_bit_identical(cfg, monkeypatch):
+    """Mesh matrices repeat a few column-offset patterns: the gather plan
+    stores a pattern start per row instead of a column index per entry
+    (k_gather_staged<PAT>); same entry order, so the same bits as the
+    explicit-index form, and the plan reports the dictionary size."""
+    a, x, _ = P.config_matrix(cfg)
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    inf = ex.info()
+    assert 0 < inf.row_patterns <= 200, inf.row_patterns
+    assert inf.stream_bytes < inf.model_bytes
+    y_pat = ex.apply(x)
+    yt_pat = ex.apply(x, transpose=True)
+    ex.close()
+    monkeypatch.setenv("CSRC_GPU_GPATTERN", "0")
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    assert ex.info().row_patterns == 0
+    assert np.array_equal(ex.apply(x), y_pat)
+    assert np.array_equal(ex.apply(x, transpose=True), yt_pat)
+    ex.close()
+    assert rel_l2(y_pat, O.spmv_csrc(a, x)) <= TOL64
+
+
+def test_permuted_mesh_has_no_small_dictionary():
+    """C3 is randomly permuted then RCM-ordered: rows do not repeat offsets,
+    the plan keeps explicit indices."""
+    a, x, _ = P.config_matrix("c3")
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    assert ex.info().row_patterns == 0
+    ex.close()
