@@ -117,6 +117,7 @@ struct csrc_gpu_plan_s {
     // row-pattern form (k_gather_pat): pattern id per row, offset table
     int gather_pat = 0;
     int gather_nt = 256;   // threads per block (k_gather_staged)
+    int gather_minb = 1;   // __launch_bounds__ min blocks (8 caps registers at 32)
     int32_t n_patterns = 0;
     DevBuf pbase, pat_off;
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
@@ -641,23 +642,27 @@ int gather_stage_smem(const Plan& P) {
 }
 
 template <class T, int L, int U, int NB>
-void* gather_stage_fn_NB(bool pat) {
-    return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true>)
-               : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false>);
+void* gather_stage_fn_NB(bool pat, int minb) {
+    if (minb == 8)
+        return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true, 8>)
+                   : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false, 8>);
+    return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true, 1>)
+               : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false, 1>);
 }
 
 template <class T, int L>
-void* gather_stage_fn_L(int U, int NB, bool pat) {
-    if (U == 8) return NB == 2 ? gather_stage_fn_NB<T, L, 8, 2>(pat) : gather_stage_fn_NB<T, L, 8, 1>(pat);
-    return NB == 2 ? gather_stage_fn_NB<T, L, 4, 2>(pat) : gather_stage_fn_NB<T, L, 4, 1>(pat);
+void* gather_stage_fn_L(int U, int NB, bool pat, int minb) {
+    if (U == 8)
+        return NB == 2 ? gather_stage_fn_NB<T, L, 8, 2>(pat, minb) : gather_stage_fn_NB<T, L, 8, 1>(pat, minb);
+    return NB == 2 ? gather_stage_fn_NB<T, L, 4, 2>(pat, minb) : gather_stage_fn_NB<T, L, 4, 1>(pat, minb);
 }
 
 template <class T>
 void* gather_stage_fn(const Plan& P) {
     switch (P.gather_lanes) {
-        case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, P.gather_pat);
-        case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, P.gather_pat);
-        default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, P.gather_pat);
+        case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
+        case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
+        default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
     }
 }
 
@@ -740,6 +745,7 @@ void setup_gather(Plan& P, const MatView& a) {
     P.gather_u = env_int("CSRC_GPU_GU", avg / P.gather_lanes <= 16 ? 8 : 4) == 8 ? 8 : 4;
     P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
     P.gather_nt = env_int("CSRC_GPU_GNT", 256) == 128 ? 128 : 256;
+    P.gather_minb = env_int("CSRC_GPU_GMINB", 1) == 8 ? 8 : 1;
     std::vector<int32_t> pbase, pat_off;
     if (env_int("CSRC_GPU_GPATTERN", 1) != 0 && P.gather_lanes <= 8)
         P.gather_pat = find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns) ? 1 : 0;
@@ -753,6 +759,10 @@ void setup_gather(Plan& P, const MatView& a) {
             if (smem <= 100 * 1024) {
                 void* fn = gather_stage_fn<T>(P);
                 CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                // shared/L1 split: the driver's choice by default (L1 serves the x gathers)
+                const int carve = env_int("CSRC_GPU_GCARVE", -1);
+                if (carve >= 0)
+                    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
                 int occ = 0;
                 CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P.gather_nt, smem));
                 if (occ >= 1) {

@@ -133,8 +133,8 @@ __host__ __device__ inline int gather_val_bytes(int cap) {
     return ((cap + 8) * static_cast<int>(sizeof(T)) + 15) & ~15;
 }
 
-template <typename T, int L, int U, int NB, bool PAT>
-__global__ void __launch_bounds__(256) k_gather_staged(const GStageArgs<T> A) {
+template <typename T, int L, int U, int NB, bool PAT, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T> A) {
     static_assert(NB == 1 || NB == 2, "one or two row-block buffers");
     extern __shared__ __align__(128) unsigned char smem[];
     const int R = blockDim.x / L;
