@@ -288,8 +288,8 @@ def main():
         from paper_1003_0952_b200.dist import DistSpmv
         ds = DistSpmv(a, strat)
         p = ds.plan
-        xd = torch.from_numpy(x[p.lo:p.row_end].copy()).to(device="cuda", dtype=tdt)
-        yd = torch.zeros_like(xd)
+        xd = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).to(device="cuda", dtype=tdt)
+        yd = torch.zeros(p.row_end - p.y_lo, device="cuda", dtype=tdt)
         dist.barrier()
         for _ in range(args.warmup):
             ds.apply_device(xd, yd)
@@ -310,9 +310,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
         kms = ms
-        launches_per_step = 3 + len(p.recvs)
+        launches_per_step = 1 if p.mode == "gather" else 3 + len(p.recvs)
         # e2e: host slice in, owned rows out
-        xh = torch.from_numpy(x[p.lo:p.row_end].copy()).pin_memory()
+        xh = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).pin_memory()
         yh = torch.empty(p.row_end - p.row_begin, dtype=torch.float64).pin_memory()
         torch.cuda.synchronize()
         dist.barrier()
@@ -320,7 +320,7 @@ def main():
         for _ in range(args.steps):
             xd.copy_(xh.to(tdt), non_blocking=True)
             ds.apply_device(xd, yd)
-            yh.copy_(yd[p.row_begin - p.lo:].to(torch.float64), non_blocking=True)
+            yh.copy_(yd[p.row_begin - p.y_lo:].to(torch.float64), non_blocking=True)
             torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.steps
         te = torch.tensor([e2e_s], device="cuda")
@@ -354,7 +354,7 @@ def main():
                       layout_frac=(layout_bytes / (kms / 1e3) / 1e9) / peak if layout_bytes else None,
                       row_patterns=row_patterns),
         e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
-                 else (p.row_end - p.lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
+                 else (p.x_hi - p.x_lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
                  else (p.row_end - p.row_begin) * 8, wall_ms_per_step=e2e_s * 1e3),
         gpu_launches=launches_per_step * args.steps,
         clocks=clocks,

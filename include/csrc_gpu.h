@@ -135,6 +135,8 @@ typedef struct {
                                    (= model_bytes for the CSRC kernels; gather: its entry
                                    stream)                          */
     int32_t row_patterns;       /* gather: column-offset patterns (0 = explicit indices) */
+    int32_t x_hi;               /* x is read on [lo, x_hi): row_end for the scatter kernels;
+                                   gather band plans also read x above the band       */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;

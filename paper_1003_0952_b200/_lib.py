@@ -82,6 +82,7 @@ class PlanInfo(C.Structure):
         ("captured_fraction", f64),
         ("stream_bytes", i64),
         ("row_patterns", i32),
+        ("x_hi", i32),
     ]
 
 

@@ -155,6 +155,7 @@ struct csrc_gpu_plan_s {
 
     size_t vsize() const { return dtype == CSRC_DTYPE_F32 ? 4 : 8; }
     index_t vec_len() const { return row_end - lo; }
+    index_t x_hi = 0;  // gather: end of the x range the plan reads (band plans: above row_end)
     int launches = 0;
 
     ~csrc_gpu_plan_s() {
@@ -668,31 +669,46 @@ void* gather_stage_fn(const Plan& P) {
 
 template <class T>
 void setup_gather(Plan& P, const MatView& a) {
-    const index_t n = a.n;
+    // rows [r0, r1) of the global matrix (the whole matrix unless a band plan);
+    // entry columns are stored in band-row coordinates (c - r0, negative below
+    // the band) and the kernels read x through a pointer shifted by r0 - lo, so
+    // the device x holds [lo, x_hi) and y holds the band rows only.
+    const index_t N = a.n;
+    const index_t r0 = P.row_begin, r1 = P.row_end;
+    const index_t n = r1 - r0;
+    const bool band = n != N;
     if (2 * static_cast<int64_t>(a.k) > INT32_MAX)
         throw Error("gather plan: more than 2^31 off-diagonal entries (use the windowed kernel)");
     std::vector<int32_t> up(static_cast<size_t>(n) + 1, 0);
-    for (count_t t = 0; t < a.k; ++t) ++up[a.ja[t] + 1];
+    index_t x_hi = r1;
+    for (index_t r = r0 + 1; r < N; ++r)
+        for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t)
+            if (a.ja[t] >= r0 && a.ja[t] < r1) {
+                ++up[a.ja[t] - r0 + 1];
+                x_hi = std::max(x_hi, r + 1);
+            }
+    P.x_hi = x_hi;
     std::vector<int32_t> eptr(static_cast<size_t>(n) + 1, 0);
     for (index_t q = 0; q < n; ++q)
-        eptr[q + 1] = eptr[q] + (a.ia[q + 1] - a.ia[q]) + up[q + 1];
+        eptr[q + 1] = eptr[q] + (a.ia[r0 + q + 1] - a.ia[r0 + q]) + up[q + 1];
     const size_t ne = static_cast<size_t>(eptr[n]);
     std::vector<int32_t> eidx(ne);
     std::vector<double> ev(ne), evt(a.value_symmetric ? 0 : ne);
     std::vector<int32_t> next(static_cast<size_t>(n));
     for (index_t q = 0; q < n; ++q) {
         int32_t w = eptr[q];
-        for (index_t t = a.ia[q]; t < a.ia[q + 1]; ++t, ++w) {
-            eidx[w] = a.ja[t];
+        for (index_t t = a.ia[r0 + q]; t < a.ia[r0 + q + 1]; ++t, ++w) {
+            eidx[w] = a.ja[t] - r0;
             ev[w] = a.al[t];
             if (!a.value_symmetric) evt[w] = a.au[t];
         }
         next[q] = w;  // upper entries of q start here
     }
-    for (index_t r = 0; r < n; ++r)  // ascending r: upper entries land sorted
+    for (index_t r = r0 + 1; r < N; ++r)  // ascending r: upper entries land sorted
         for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) {
-            const int32_t w = next[a.ja[t]]++;
-            eidx[w] = r;
+            if (a.ja[t] < r0 || a.ja[t] >= r1) continue;
+            const int32_t w = next[a.ja[t] - r0]++;
+            eidx[w] = r - r0;
             ev[w] = a.value_symmetric ? a.al[t] : a.au[t];
             if (!a.value_symmetric) evt[w] = a.al[t];
         }
@@ -704,7 +720,7 @@ void setup_gather(Plan& P, const MatView& a) {
     P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? 2 : avg <= 128 ? 4 : 8);
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
     P.gather_bpsm = env_int("CSRC_GPU_GBPSM", 16);  // 256-thread blocks per SM
-    {
+    if (!band) {
         // host pipeline: row chunks on multiples of 256 rows (any lane count's block).
         // Ramped sizes (in 64ths of n): a small first chunk starts the y download
         // early, small last chunks shorten the compute + download tail after the
@@ -810,6 +826,7 @@ template <class T>
 void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, int32_t r1,
                          cudaStream_t st) {
     if (r1 <= r0) return;
+    x += P.row_begin - P.lo;  // band plans: x holds [lo, x_hi), columns are band-row relative
     const T* vals = (tr && !P.value_symmetric ? P.eval_t : P.eval).template as<T>();
     if (P.gather_buf) {
         const int R = P.gather_nt / P.gather_lanes;
@@ -987,9 +1004,8 @@ Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const C
     const int single = o.band ? CSRC_KIND_WINDOWED : CSRC_KIND_GATHER;
     if (s->kind == CSRC_KIND_SEQUENTIAL) P->exec_kind = single;
     if (s->kind == CSRC_KIND_LOCAL_BUFFERS && s->p < 2 && !o.block_start) P->exec_kind = single;
-    if (o.band && (P->exec_kind == CSRC_KIND_LOCAL_BUFFERS || P->exec_kind == CSRC_KIND_COLORFUL ||
-                   P->exec_kind == CSRC_KIND_GATHER))
-        throw Error("band plans support the windowed and atomic kernels only");
+    if (o.band && (P->exec_kind == CSRC_KIND_LOCAL_BUFFERS || P->exec_kind == CSRC_KIND_COLORFUL))
+        throw Error("band plans support the windowed, atomic and gather kernels only");
     CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
     for (auto& e : P->ev) CUDA_OK(cudaEventCreate(&e));
     if (a.n == 0) return P.release();
@@ -1076,6 +1092,8 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
     T* y = static_cast<T*>(dy);
     const size_t ybytes = static_cast<size_t>(P.vec_len()) * sizeof(T);
     if (part >= 0) {
+        if (P.exec_kind != CSRC_KIND_WINDOWED)
+            throw Error("boundary / interior parts need a windowed band plan");
         // band plan partial products
         if (part == 0) CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
         auto A = win_args<T>(P, dx, dy, tr);
@@ -1407,6 +1425,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         info->captured_fraction = P.captured;
         info->stream_bytes = info->model_bytes;
         info->row_patterns = 0;
+        info->x_hi = P.exec_kind == CSRC_KIND_GATHER ? P.x_hi : P.row_end;
         if (P.exec_kind == CSRC_KIND_GATHER) {
             const int64_t ne = P.nrows ? static_cast<int64_t>(2) * P.k : 0;
             const int64_t vs = static_cast<int64_t>(P.vsize());

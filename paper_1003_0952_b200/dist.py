@@ -1,4 +1,13 @@
-"""Multi-GPU CSRC product: one process per GPU, row bands, halo reduce.
+"""Multi-GPU CSRC product: one process per GPU, row bands.
+
+Two band forms:
+
+* gather (default): rank g runs the gather kernel on its rows
+  [block_start[g], block_start[g+1]); a row reads x below the band (its lower
+  pairs) and above it (the rows that name it as a column), so x is replicated
+  over [lo_g, x_hi_g) and the rank writes exactly its own y rows: no y
+  exchange at all (weak-scaling shards, no data-path collective).
+* windowed (scatter): the y-halo reduce below.
 
 Rank g owns rows [block_start[g], block_start[g+1]) of
 ``partition_by_nnz(a, world)`` (partition.hpp:55-90, bit-exact) and computes
@@ -47,6 +56,20 @@ class HaloPlan:
     sends: List[Tuple[int, int, int]]
     # (peer, q0, q1): global positions [q0, q1) of my rows in peer's halo
     recvs: List[Tuple[int, int, int]]
+    # device vectors: x_local covers [x_lo, x_hi), y_local covers [y_lo, row_end)
+    x_hi: int = -1
+    y_lo: int = -1
+    mode: str = "windowed"
+
+    def __post_init__(self):
+        if self.x_hi < 0:
+            self.x_hi = self.row_end
+        if self.y_lo < 0:
+            self.y_lo = self.lo
+
+    @property
+    def x_lo(self) -> int:
+        return self.lo
 
     @property
     def vec_len(self) -> int:
@@ -56,6 +79,23 @@ class HaloPlan:
         s = sum(q1 - q0 for _, q0, q1 in self.sends) * elem
         r = sum(q1 - q0 for _, q0, q1 in self.recvs) * elem
         return s, r
+
+
+def band_x_hi(a: CsrcMatrix, r0: int, r1: int) -> int:
+    """End of the x range rows [r0, r1) read in the gather form: one past the
+    last row r whose stored pairs name a column in [r0, r1)."""
+    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.ia))
+    m = (a.ja >= r0) & (a.ja < r1)
+    return int(max(r1, rows[m].max() + 1)) if m.any() else int(r1)
+
+
+def gather_plan(a: CsrcMatrix, world: int, rank: int, x_hi: Optional[int] = None) -> HaloPlan:
+    """Gather-form band of rank `rank`: no exchange, x over [lo, x_hi)."""
+    part = partition_by_nnz(a, world)
+    ranges = effective_ranges(a, part)
+    r0, r1 = part.begin(rank), part.end(rank)
+    hi = band_x_hi(a, r0, r1) if x_hi is None else x_hi
+    return HaloPlan(rank, world, r0, r1, ranges[rank].lo, [], [], x_hi=hi, y_lo=r0, mode="gather")
 
 
 def halo_plan(a: CsrcMatrix, world: int, rank: int) -> HaloPlan:
@@ -79,9 +119,11 @@ def halo_plan(a: CsrcMatrix, world: int, rank: int) -> HaloPlan:
 class DistSpmv:
     """Band-decomposed product on the current process group.
 
-    Device mode: x_local / y_local are CUDA tensors covering global positions
-    [plan.lo, plan.row_end); after ``apply_device`` the owned rows
-    y_local[row_begin - lo:] hold the final product rows.
+    Device mode: x_local covers global positions [plan.x_lo, plan.x_hi),
+    y_local [plan.y_lo, plan.row_end) (CUDA tensors); after ``apply_device``
+    the owned rows y_local[row_begin - y_lo:] hold the final product rows.
+    Gather form: y_lo = row_begin, x_hi above the band; windowed form:
+    x_lo = y_lo = lo, x_hi = row_end.
     """
 
     def __init__(self, a: CsrcMatrix, strategy: Optional[Strategy] = None, group=None,
@@ -92,16 +134,25 @@ class DistSpmv:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.plan = halo_plan(a, self.world, self.rank)
+        s = strategy or Strategy(StrategyKind.gather)
+        if s.kind in (StrategyKind.sequential, StrategyKind.local_buffers, StrategyKind.colorful):
+            s = dataclasses.replace(s, kind=StrategyKind.gather)  # band forms: gather or scatter
+        self.mode = "gather" if s.kind == StrategyKind.gather else "windowed"
         self.band_compute = band_compute
         self.ex = None
-        if band_compute is None:
-            s = strategy or Strategy(StrategyKind.windowed)
-            if s.kind == StrategyKind.gather:
-                # the gather kernel reads x above the band (x halo, not y halo);
-                # band plans use the scatter form whose exchange is the y halo
-                s = dataclasses.replace(s, kind=StrategyKind.windowed)
-            self.ex = GpuSpmv(a, s, band=(self.plan.row_begin, self.plan.row_end))
+        if self.mode == "gather":
+            part = partition_by_nnz(a, self.world)
+            r0, r1 = part.begin(self.rank), part.end(self.rank)
+            x_hi = None
+            if band_compute is None:
+                self.ex = GpuSpmv(a, s, band=(r0, r1))
+                x_hi = int(self.ex.info().x_hi)
+            self.plan = gather_plan(a, self.world, self.rank, x_hi)
+        else:
+            self.plan = halo_plan(a, self.world, self.rank)
+            if band_compute is None:
+                self.ex = GpuSpmv(a, s, band=(self.plan.row_begin, self.plan.row_end))
+        if self.ex is not None:
             assert self.ex.info().lo == self.plan.lo
         self._bufs = None
         self._streams = None
@@ -128,6 +179,8 @@ class DistSpmv:
 
         p = self.plan
         y_local.copy_(torch.as_tensor(self.band_compute(p, x_local.numpy())))
+        if self.mode == "gather":
+            return y_local  # own rows only, nothing to exchange
         recv_bufs = [torch.empty(q1 - q0, dtype=y_local.dtype) for _, q0, q1 in p.recvs]
         for w in self._post(y_local, recv_bufs):
             w.wait()
@@ -139,6 +192,9 @@ class DistSpmv:
         import torch
 
         p = self.plan
+        if self.mode == "gather":
+            self.ex.apply_device(x_local, y_local)
+            return y_local
         if self._streams is None:
             self._streams = (torch.cuda.current_stream(), torch.cuda.Stream())
             self._bufs = [torch.empty(q1 - q0, dtype=y_local.dtype, device=y_local.device)
@@ -173,7 +229,7 @@ class DistSpmv:
 def gather_product(plan: HaloPlan, y_local, world_y: Optional[np.ndarray] = None):
     """Owned rows of y_local as numpy (rows [row_begin, row_end))."""
     arr = y_local.detach().cpu().numpy() if hasattr(y_local, "detach") else np.asarray(y_local)
-    own = arr[plan.row_begin - plan.lo:]
+    own = arr[plan.row_begin - plan.y_lo:]
     if world_y is not None:
         world_y[plan.row_begin:plan.row_end] = own
     return own

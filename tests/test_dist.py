@@ -1,7 +1,9 @@
-"""Multi-rank path on CPU (gloo, world size 2 and 3): the halo plan and the
-P2P exchange of paper_1003_0952_b200.dist reassemble the full product; the
-band product itself is injected from the oracle here (on the GPU box the band
-plans of the windowed kernel do it; tests/test_gpu_parity.py checks those)."""
+"""Multi-rank path on CPU (gloo, world size 2 and 3): the band forms of
+paper_1003_0952_b200.dist reassemble the full product — the windowed form
+through its halo plan and P2P exchange, the gather form with no exchange (x
+replicated over [lo, x_hi)). The band product itself is injected from the
+oracle here (on the GPU box the band plans do it; tests/test_gpu_parity.py
+checks those)."""
 import os
 import socket
 
@@ -10,7 +12,7 @@ import pytest
 import torch.multiprocessing as mp
 
 import paper_1003_0952_b200 as P
-from paper_1003_0952_b200.dist import halo_plan
+from paper_1003_0952_b200.dist import band_x_hi, gather_plan, halo_plan
 
 from .helpers import meshes
 
@@ -39,7 +41,15 @@ def _band_product(a, plan, x_local):
     return Oracle().spmv_csrc(sub, x)[plan.lo:plan.row_end]
 
 
-def _worker(rank, world, port, mesh_key, out_q):
+def _gather_band_product(a, plan, x_local):
+    """Oracle product of rows [row_begin, row_end) from x on [lo, x_hi)."""
+    from oracle.oracle import Oracle
+    x = np.zeros(a.n)
+    x[plan.x_lo:plan.x_hi] = x_local
+    return Oracle().spmv_csrc(a, x)[plan.row_begin:plan.row_end]
+
+
+def _worker(rank, world, port, mesh_key, out_q, mode="windowed"):
     import torch
     import torch.distributed as dist
     from paper_1003_0952_b200.dist import DistSpmv
@@ -51,23 +61,27 @@ def _worker(rank, world, port, mesh_key, out_q):
         m = meshes()
         a = m.matrix(mesh_key)
         x = m[mesh_key + "x"]
-        ds = DistSpmv(a, band_compute=lambda plan, xl: _band_product(a, plan, xl))
+        fn = _gather_band_product if mode == "gather" else _band_product
+        s = P.Strategy(P.StrategyKind.gather if mode == "gather" else P.StrategyKind.windowed)
+        ds = DistSpmv(a, s, band_compute=lambda plan, xl: fn(a, plan, xl))
         p = ds.plan
-        xl = torch.from_numpy(x[p.lo:p.row_end].copy())
-        yl = torch.zeros_like(xl)
+        assert p.mode == mode
+        xl = torch.from_numpy(x[p.x_lo:p.x_hi].copy())
+        yl = torch.zeros(p.row_end - p.y_lo, dtype=torch.float64)
         ds.apply_host(xl, yl)
-        out_q.put((rank, p.row_begin, p.row_end, yl.numpy()[p.row_begin - p.lo:].copy()))
+        out_q.put((rank, p.row_begin, p.row_end, yl.numpy()[p.row_begin - p.y_lo:].copy()))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["windowed", "gather"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("mesh_key", ["g1_", "g3_", "g5_"])
-def test_gloo_band_exchange_reassembles_the_product(world, mesh_key):
+def test_gloo_band_exchange_reassembles_the_product(world, mesh_key, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_key, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_key, q, mode)) for r in range(world)]
     for pr in procs:
         pr.start()
     parts = [q.get(timeout=120) for _ in range(world)]
@@ -94,3 +108,20 @@ def test_halo_plan_is_consistent_across_ranks():
         for p in plans:
             for peer, q0, q1 in p.sends:
                 assert peer < p.rank and plans[peer].row_begin <= q0 < q1 <= plans[peer].row_end
+
+
+def test_gather_plan_ranges():
+    """Gather bands: no exchange; x range covers every column the band's rows
+    read (lower pairs down to lo, upper pairs up to x_hi - 1)."""
+    m = meshes()
+    a = m.matrix("g3_")
+    rows = np.repeat(np.arange(a.n), np.diff(a.ia))
+    for world in (2, 3, 5):
+        for r in range(world):
+            p = gather_plan(a, world, r)
+            assert not p.sends and not p.recvs and p.y_lo == p.row_begin
+            lower = a.ja[a.ia[p.row_begin]:a.ia[p.row_end]]
+            assert lower.size == 0 or lower.min() >= p.x_lo
+            upper_rows = rows[(a.ja >= p.row_begin) & (a.ja < p.row_end)]
+            assert upper_rows.size == 0 or upper_rows.max() < p.x_hi
+            assert p.x_hi == band_x_hi(a, p.row_begin, p.row_end) >= p.row_end

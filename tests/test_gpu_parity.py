@@ -286,6 +286,20 @@ def test_band_plans_assemble_the_product(bands, mesh):
     part = P.partition_by_nnz(a, bands)
     y = np.zeros(a.n)
     xd_full = torch.from_numpy(x).cuda()
+    for b in range(bands):  # gather form: x over [lo, x_hi), own rows only, no exchange
+        r0, r1 = part.begin(b), part.end(b)
+        ex = P.GpuSpmv(a, P.Strategy(K.gather), band=(r0, r1))
+        inf = ex.info()
+        assert inf.lo <= r0 and inf.x_hi >= r1
+        yd = torch.full((r1 - r0,), float("nan"), dtype=torch.float64, device="cuda")
+        ex.apply_device(xd_full[inf.lo:inf.x_hi].contiguous(), yd)
+        torch.cuda.synchronize()
+        y[r0:r1] = yd.cpu().numpy()
+        with pytest.raises(P.Error, match="partial products need the windowed kernel"):
+            ex.apply_device_part(xd_full, yd, 0)
+        ex.close()
+    assert rel_l2(y, MESH[mesh + "y"]) <= TOL64
+    y = np.zeros(a.n)
     for b in range(bands):
         r0, r1 = part.begin(b), part.end(b)
         ex = P.GpuSpmv(a, P.Strategy(K.windowed), band=(r0, r1))
