@@ -137,6 +137,8 @@ typedef struct {
     int32_t row_patterns;       /* gather: column-offset patterns (0 = explicit indices) */
     int32_t x_hi;               /* x is read on [lo, x_hi): row_end for the scatter kernels;
                                    gather band plans also read x above the band       */
+    int32_t m_cols;             /* rectangular plans: columns of A (x length); 0 = square */
+    int64_t rect_nnz;           /* rectangular plans: entries of the CSR tail        */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;
@@ -174,6 +176,16 @@ int csrc_gpu_plan_create_partitioned(const csrc_host_matrix* a, const csrc_gpu_s
  * (still missing the halo partials of higher bands). */
 int csrc_gpu_plan_create_band(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                               int32_t row_begin, int32_t row_end, csrc_gpu_plan_t* out);
+
+/* ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181) and
+ * spmv_csrc_rect (kernels.hpp:69-91): the n x n CSRC part `a` plus the CSR
+ * tail over columns n..m_cols-1 (tail_row_ptr[n+1], local column indices,
+ * csrc_matrix.hpp:35-39). x has m_cols entries; every kernel kind runs its
+ * square product, then one tail pass adds the row sums of the tail. No
+ * transpose product and no band plans for rectangular matrices. */
+int csrc_gpu_plan_create_rect(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t m_cols,
+                              const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
+                              const double* tail_values, csrc_gpu_plan_t* out);
 
 void csrc_gpu_plan_destroy(csrc_gpu_plan_t plan);
 int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info);
@@ -272,6 +284,47 @@ int csrc_colorful_slices(const csrc_host_matrix* a, const int32_t* color, int32_
  * (cost_model.hpp:67-89, Format::csrc / csrc_sym). */
 int64_t csrc_model_bytes(int64_t n, int64_t nnz_stored, int32_t value_symmetric, int32_t dtype);
 int64_t csrc_model_flops(int64_t n, int64_t nnz_full);
+
+/* ------------------------------------------------ CSRC construction
+ * Device re-implementations of the reference's construction pipeline
+ * (paper_1003_0952_b200/csrc/assemble.cu). Results are host arrays owned by
+ * the returned handle, bit-exact with the reference (tests/test_gpu_assemble.py):
+ * values are copies of input values, duplicates summed in input order. */
+typedef struct csrc_built_s* csrc_built_t;
+
+/* build_csr (csr.hpp:55-92): canonical CSR from m triplets (rows[e], cols[e],
+ * vals[e]); duplicates summed; "build_csr: entry (r, c) outside RxC bounds"
+ * names the first out-of-bounds triplet in input order. */
+int csrc_gpu_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t* rows,
+                       const int32_t* cols, const double* vals, int32_t device, csrc_built_t* out);
+
+/* csr_to_csrc(build_csr(t)) (csrc_matrix.hpp:44-91) without the host round
+ * trip: "csr_to_csrc: entry (i, j) has no transpose (j, i)" / "row i has no
+ * diagonal entry" report the first failure in the reference's row-major order;
+ * value_symmetric set (and au dropped) iff every pair matches exactly. */
+int csrc_gpu_build_csrc(int32_t n, int64_t m, const int32_t* rows, const int32_t* cols,
+                        const double* vals, int32_t device, csrc_built_t* out);
+
+/* csr_to_csrc (csrc_matrix.hpp:44-91) of a canonical CSR. */
+int csrc_gpu_csr_to_csrc(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
+                         const int32_t* col_idx, const double* values, int32_t device,
+                         csrc_built_t* out);
+
+/* decompose_rect (csrc_matrix.hpp:113-142, symmetrize = false): CSRC square
+ * part + CSR tail over columns n..m-1 (local indices). */
+int csrc_gpu_decompose_rect(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
+                            const int32_t* col_idx, const double* values, int32_t device,
+                            csrc_built_t* out);
+
+/* Views into a handle (valid until csrc_built_free). */
+int csrc_built_matrix(csrc_built_t b, csrc_host_matrix* m);
+int csrc_built_csr(csrc_built_t b, int32_t* n_rows, int32_t* n_cols, int64_t* nnz,
+                   const int32_t** row_ptr, const int32_t** col_idx, const double** values);
+int csrc_built_rect_tail(csrc_built_t b, int32_t* m_cols, int64_t* nnz, const int32_t** row_ptr,
+                         const int32_t** col_idx, const double** values);
+/* wall-clock ms of the phases: [0] H2D, [1] sort + reduce, [2] CSR -> CSRC, [3] D2H */
+int csrc_built_timings(csrc_built_t b, double* ms4);
+void csrc_built_free(csrc_built_t b);
 
 /* --------------------------------------------------------- fixtures
  * Deterministic synthetic FE matrices for the BASELINE configs, assembled

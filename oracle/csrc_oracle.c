@@ -41,6 +41,26 @@ void oracle_spmv_csrc(index_t n, const double* ad, const index_t* ia, const inde
     }
 }
 
+/* spmv_csrc_rect, kernels.hpp:69-91: per row the square CSRC updates, then
+ * the CSR tail over x[n + tcol] (x has length m). */
+void oracle_spmv_csrc_rect(index_t n, const double* ad, const index_t* ia, const index_t* ja,
+                           const double* al, const double* au, const index_t* trp,
+                           const index_t* tci, const double* tva, const double* x, double* y) {
+    const double* up = au ? au : al;
+    memset(y, 0, sizeof(double) * (size_t)n);
+    for (index_t i = 0; i < n; ++i) {
+        const double xi = x[i];
+        double yi = ad[i] * xi;
+        for (index_t t = ia[i]; t < ia[i + 1]; ++t) {
+            const index_t j = ja[t];
+            yi += al[t] * x[j];
+            y[j] += up[t] * xi;
+        }
+        for (index_t q = trp[i]; q < trp[i + 1]; ++q) yi += tva[q] * x[n + tci[q]];
+        y[i] = yi;
+    }
+}
+
 /* spmv_csrc_transpose, kernels.hpp:47-65: al and au swap roles. */
 void oracle_spmv_csrc_transpose(index_t n, const double* ad, const index_t* ia,
                                 const index_t* ja, const double* al, const double* au,

@@ -63,6 +63,19 @@ class Oracle:
            _p(a.al, C.c_double), _p(au, C.c_double), _p(x, C.c_double), _p(y, C.c_double))
         return y
 
+    def spmv_csrc_rect(self, r, x):
+        """spmv_csrc_rect (kernels.hpp:69-91); r has .square, .rect, .m."""
+        a, t = r.square, r.rect
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(a.n, np.float64)
+        au = None if a.value_symmetric else a.au
+        self.lib.oracle_spmv_csrc_rect(
+            C.c_int32(a.n), _p(a.ad, C.c_double), _p(a.ia, C.c_int32), _p(a.ja, C.c_int32),
+            _p(a.al, C.c_double), _p(au, C.c_double), _p(np.ascontiguousarray(t.row_ptr, np.int32), C.c_int32),
+            _p(np.ascontiguousarray(t.col_idx, np.int32), C.c_int32),
+            _p(np.ascontiguousarray(t.values, np.float64), C.c_double), _p(x, C.c_double), _p(y, C.c_double))
+        return y
+
     def spmv_local_buffers(self, a, x, block_start):
         x = np.ascontiguousarray(x, np.float64)
         p = len(block_start) - 1
@@ -255,6 +268,63 @@ class Ref:
                                 _p(al, C.c_double), _p(au, C.c_double))
         return dict(n=n, ad=ad, ia=ia, ja=ja[:kk].copy(), al=al[:kk].copy(),
                     au=np.zeros(0) if vs.value else au[:kk].copy(), value_symmetric=bool(vs.value))
+
+    def build_csr(self, n_rows, n_cols, rows, cols, vals):
+        """build_csr (csr.hpp:55-92) -> (row_ptr, col_idx, values)."""
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = np.ascontiguousarray(vals, np.float64)
+        self._chk(self.lib.ref_build_csr(C.c_int32(n_rows), C.c_int32(n_cols), C.c_int64(rows.size),
+                                         _p(rows, C.c_int32), _p(cols, C.c_int32), _p(vals, C.c_double)))
+        return self._csr_out()
+
+    def _csr_out(self):
+        nr, nc, nnz = C.c_int32(), C.c_int32(), C.c_int64()
+        self.lib.ref_csr_sizes(C.byref(nr), C.byref(nc), C.byref(nnz))
+        rp = np.zeros(nr.value + 1, np.int32)
+        ci = np.zeros(max(nnz.value, 1), np.int32)
+        va = np.zeros(max(nnz.value, 1), np.float64)
+        self.lib.ref_csr_copy(_p(rp, C.c_int32), _p(ci, C.c_int32), _p(va, C.c_double))
+        return rp, ci[: nnz.value].copy(), va[: nnz.value].copy()
+
+    def _built_out(self):
+        nn, k, vs = C.c_int32(), C.c_int64(), C.c_int32()
+        self.lib.ref_built_sizes(C.byref(nn), C.byref(k), C.byref(vs))
+        n, kk = nn.value, k.value
+        ad = np.zeros(max(n, 1), np.float64)
+        ia = np.zeros(n + 1, np.int32)
+        ja = np.zeros(max(kk, 1), np.int32)
+        al = np.zeros(max(kk, 1), np.float64)
+        au = np.zeros(max(kk, 1), np.float64)
+        self.lib.ref_built_copy(_p(ad, C.c_double), _p(ia, C.c_int32), _p(ja, C.c_int32),
+                                _p(al, C.c_double), _p(au, C.c_double))
+        return dict(n=n, ad=ad[:n].copy(), ia=ia, ja=ja[:kk].copy(), al=al[:kk].copy(),
+                    au=np.zeros(0) if vs.value else au[:kk].copy(), value_symmetric=bool(vs.value))
+
+    def decompose_rect(self, n_rows, n_cols, rp, ci, va):
+        """decompose_rect (csrc_matrix.hpp:113-142) -> (square dict, (trp, tci, tva))."""
+        rp = np.ascontiguousarray(rp, np.int32)
+        ci = np.ascontiguousarray(ci, np.int32)
+        va = np.ascontiguousarray(va, np.float64)
+        self._chk(self.lib.ref_decompose_rect(C.c_int32(n_rows), C.c_int32(n_cols), _p(rp, C.c_int32),
+                                              _p(ci, C.c_int32), _p(va, C.c_double)))
+        return self._built_out(), self._csr_out()
+
+    def spmv_csrc_rect(self, r, x):
+        """spmv_csrc_rect (kernels.hpp:69-91) of the reference itself."""
+        a, t = r.square, r.rect
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(a.n, np.float64)
+        au = None if a.value_symmetric else a.au
+        trp = np.ascontiguousarray(t.row_ptr, np.int32)
+        tci = np.ascontiguousarray(t.col_idx, np.int32)
+        tva = np.ascontiguousarray(t.values, np.float64)
+        self._chk(self.lib.ref_spmv_csrc_rect(
+            C.c_int32(a.n), C.c_int64(a.ja.size), _p(a.ad, C.c_double), _p(a.ia, C.c_int32),
+            _p(a.ja, C.c_int32), _p(a.al, C.c_double), _p(au, C.c_double),
+            C.c_int32(int(a.value_symmetric)), C.c_int32(r.m), _p(trp, C.c_int32), _p(tci, C.c_int32),
+            _p(tva, C.c_double), _p(x, C.c_double), C.c_int64(x.size), _p(y, C.c_double)))
+        return y
 
     def spmv_csrc(self, a, x, transpose=False):
         x = np.ascontiguousarray(x, np.float64)

@@ -89,6 +89,65 @@ void ref_built_copy(double* ad, int32_t* ia, int32_t* ja, double* al, double* au
         std::memcpy(au, g_built.au.data(), sizeof(double) * g_built.au.size());
 }
 
+// build_csr (csr.hpp:55-92) alone; results fetched with ref_csr_sizes / ref_csr_copy.
+CsrMatrix g_csr;
+int ref_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t* rows,
+                  const int32_t* cols, const double* vals) {
+    return guarded([&] {
+        TripletMatrix t;
+        t.n_rows = n_rows;
+        t.n_cols = n_cols;
+        for (int64_t e = 0; e < m; ++e) t.add(rows[e], cols[e], vals[e]);
+        g_csr = build_csr(t);
+    });
+}
+void ref_csr_sizes(int32_t* n_rows, int32_t* n_cols, int64_t* nnz) {
+    *n_rows = g_csr.n_rows;
+    *n_cols = g_csr.n_cols;
+    *nnz = g_csr.nnz();
+}
+void ref_csr_copy(int32_t* rp, int32_t* ci, double* va) {
+    std::memcpy(rp, g_csr.row_ptr.data(), sizeof(int32_t) * g_csr.row_ptr.size());
+    std::memcpy(ci, g_csr.col_idx.data(), sizeof(int32_t) * g_csr.col_idx.size());
+    std::memcpy(va, g_csr.values.data(), sizeof(double) * g_csr.values.size());
+}
+
+// decompose_rect (csrc_matrix.hpp:113-142): square part -> ref_built_*, tail -> ref_csr_*.
+int ref_decompose_rect(int32_t n_rows, int32_t n_cols, const int32_t* rp, const int32_t* ci,
+                       const double* va) {
+    return guarded([&] {
+        CsrMatrix a;
+        a.n_rows = n_rows;
+        a.n_cols = n_cols;
+        a.row_ptr.assign(rp, rp + n_rows + 1);
+        a.col_idx.assign(ci, ci + rp[n_rows]);
+        a.values.assign(va, va + rp[n_rows]);
+        CsrcRectMatrix r = decompose_rect(a);
+        g_built = r.square;
+        g_csr = r.rect;
+    });
+}
+
+// spmv_csrc_rect (kernels.hpp:69-91).
+int ref_spmv_csrc_rect(int32_t n, int64_t k, const double* ad, const int32_t* ia,
+                       const int32_t* ja, const double* al, const double* au, int32_t vs,
+                       int32_t m_cols, const int32_t* trp, const int32_t* tci, const double* tva,
+                       const double* x, int64_t x_len, double* y) {
+    return guarded([&] {
+        CsrcRectMatrix r;
+        r.square = make(n, k, ad, ia, ja, al, au, vs);
+        r.rect.n_rows = n;
+        r.rect.n_cols = m_cols - n;
+        r.rect.row_ptr.assign(trp, trp + n + 1);
+        r.rect.col_idx.assign(tci, tci + trp[n]);
+        r.rect.values.assign(tva, tva + trp[n]);
+        r.m = m_cols;
+        Vector xv(x, x + x_len);
+        Vector out = spmv_csrc_rect(r, xv);
+        std::memcpy(y, out.data(), sizeof(double) * n);
+    });
+}
+
 // generate.hpp:12-65 families -> triplets (fetched with ref_trip_*)
 int ref_gen_random_sym(int32_t n, double density, uint64_t seed, int32_t vs) {
     return guarded([&] { g_trip = generate_random_sym(n, density, seed, vs != 0); });

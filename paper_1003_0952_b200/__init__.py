@@ -22,6 +22,10 @@ reference (file:line)                  here
 ``LocalBuffersPlan`` parallel.hpp:40-52  :class:`LocalBuffersPlan`
 ``working_set_kb`` working_set.hpp:17    :func:`working_set_kb`
 ``count_ops`` cost_model.hpp:67          :func:`model_flops`
+``build_csr`` csr.hpp:55-92              :func:`build_csr` (device, construct.py)
+``csr_to_csrc`` csrc_matrix.hpp:44-91    :func:`csr_to_csrc`, :func:`build_csrc`
+``decompose_rect`` csrc_matrix.hpp:113   :func:`decompose_rect`
+``spmv_csrc_rect`` kernels.hpp:69-91     :func:`spmv_csrc_rect`; ``GpuSpmv(CsrcRectMatrix, s)``
 =====================================  =============================================
 
 Errors raise :class:`Error` (``csrc::Error``, common.hpp:15-18) with the
@@ -46,7 +50,8 @@ __all__ = [
     "IntervalPlan", "Coloring", "ColoringValidity", "color_rows", "validate_coloring",
     "conflict_edge_counts", "ColorfulPlan", "LocalBuffersPlan", "working_set_kb",
     "model_bytes", "model_flops", "Mesh", "generate_fixture", "CONFIGS", "config_matrix",
-    "fixture_u01",
+    "fixture_u01", "TripletMatrix", "CsrMatrix", "CsrcRectMatrix", "build_csr", "build_csrc",
+    "csr_to_csrc", "decompose_rect", "csrc_to_triplets", "spmv_csrc_rect",
 ]
 
 
@@ -377,14 +382,28 @@ class GpuSpmv:
     raw ints) and enqueues asynchronously on a CUDA stream.
     """
 
-    def __init__(self, a: CsrcMatrix, strategy: Strategy = Strategy(), plan=None,
+    def __init__(self, a, strategy: Strategy = Strategy(), plan=None,
                  band: Optional[Tuple[int, int]] = None):
+        rect = a if isinstance(a, CsrcRectMatrix) else None
+        if rect is not None:
+            a = rect.square
         self._a_n = a.n
         self.strategy = strategy
         self._h = C.c_void_p()
         cm = a._c()
         s = strategy._c()
-        if isinstance(plan, ColorfulPlan):
+        if rect is not None:
+            # ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181)
+            if plan is not None or band is not None:
+                raise Error("rectangular plans take no explicit plan or band")
+            trp = _as(rect.rect.row_ptr, np.int32)
+            tci = _as(rect.rect.col_idx, np.int32)
+            tva = _as(rect.rect.values, np.float64)
+            self._keep_rect = (trp, tci, tva)
+            rc = L.plan_create_rect(C.byref(cm), C.byref(s), int(rect.m), trp.ctypes.data_as(L.P_i32),
+                                    tci.ctypes.data_as(L.P_i32) if tci.size else None,
+                                    tva.ctypes.data_as(L.P_f64) if tva.size else None, C.byref(self._h))
+        elif isinstance(plan, ColorfulPlan):
             color = _as(plan.coloring.color, np.int32)
             rc = L.plan_create_colored(C.byref(cm), C.byref(s), color.ctypes.data_as(L.P_i32),
                                        plan.coloring.n_colors, C.byref(self._h))
@@ -517,6 +536,18 @@ def spmv_csrc(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarray:
         ex.close()
 
 
+def spmv_csrc_rect(a, x, dtype: DType = DType.f64) -> np.ndarray:
+    """spmv_csrc_rect (kernels.hpp:69-91): CSRC square part + CSR tail; x has m entries."""
+    xv = _as(x, np.float64)
+    if xv.size != a.m:
+        raise Error(f"spmv_csrc_rect: x has length {xv.size}, expected {a.m}")
+    ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype))
+    try:
+        return ex.apply(xv)
+    finally:
+        ex.close()
+
+
 def spmv_csrc_transpose(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarray:
     """spmv_csrc_transpose (kernels.hpp:47-65): al/au swapped, zero-copy."""
     xv = _as(x, np.float64)
@@ -591,3 +622,9 @@ def config_matrix(name: str, threads: int = 0):
     c = CONFIGS[name]
     return generate_fixture(c["mesh"], c["nx"], c["ny"], c["nz"], c["seed"], c["diag_base"],
                             threads)
+
+
+from .construct import (  # noqa: E402  (needs Error / CsrcMatrix defined above)
+    CsrMatrix, CsrcRectMatrix, TripletMatrix, build_csr, build_csrc, csr_to_csrc, csrc_to_triplets,
+    decompose_rect,
+)

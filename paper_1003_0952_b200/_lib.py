@@ -83,6 +83,8 @@ class PlanInfo(C.Structure):
         ("stream_bytes", i64),
         ("row_patterns", i32),
         ("x_hi", i32),
+        ("m_cols", i32),
+        ("rect_nnz", i64),
     ]
 
 
@@ -117,6 +119,8 @@ plan_create_partitioned = _sig(
     "csrc_gpu_plan_create_partitioned", C.c_int, PM, PS, P_i32, i32, C.POINTER(vp)
 )
 plan_create_band = _sig("csrc_gpu_plan_create_band", C.c_int, PM, PS, i32, i32, C.POINTER(vp))
+plan_create_rect = _sig("csrc_gpu_plan_create_rect", C.c_int, PM, PS, i32, P_i32, P_i32, P_f64,
+                        C.POINTER(vp))
 plan_destroy = _sig("csrc_gpu_plan_destroy", None, vp)
 plan_get_info = _sig("csrc_gpu_plan_get_info", C.c_int, vp, C.POINTER(PlanInfo))
 spmv = _sig("csrc_gpu_spmv", C.c_int, vp, P_f64, i64, P_f64)
@@ -152,10 +156,23 @@ fixture_order = _sig("csrc_fixture_order", P_i32, vp)
 fixture_free = _sig("csrc_fixture_free", None, vp)
 fixture_u01 = _sig("csrc_fixture_u01", f64, u64, u64, u64)
 
+build_csr = _sig("csrc_gpu_build_csr", C.c_int, i32, i32, i64, P_i32, P_i32, P_f64, i32, C.POINTER(vp))
+build_csrc = _sig("csrc_gpu_build_csrc", C.c_int, i32, i64, P_i32, P_i32, P_f64, i32, C.POINTER(vp))
+csr_to_csrc = _sig("csrc_gpu_csr_to_csrc", C.c_int, i32, i32, P_i32, P_i32, P_f64, i32, C.POINTER(vp))
+decompose_rect = _sig("csrc_gpu_decompose_rect", C.c_int, i32, i32, P_i32, P_i32, P_f64, i32,
+                      C.POINTER(vp))
+built_matrix = _sig("csrc_built_matrix", C.c_int, vp, PM)
+built_csr = _sig("csrc_built_csr", C.c_int, vp, P_i32, P_i32, P_i64, C.POINTER(P_i32),
+                 C.POINTER(P_i32), C.POINTER(P_f64))
+built_rect_tail = _sig("csrc_built_rect_tail", C.c_int, vp, P_i32, P_i64, C.POINTER(P_i32),
+                       C.POINTER(P_i32), C.POINTER(P_f64))
+built_timings = _sig("csrc_built_timings", C.c_int, vp, P_f64)
+built_free = _sig("csrc_built_free", None, vp)
+
 EXPORTED = [
     "csrc_gpu_last_error", "csrc_gpu_abi_version", "csrc_gpu_device_count",
     "csrc_gpu_plan_create", "csrc_gpu_plan_create_colored", "csrc_gpu_plan_create_partitioned",
-    "csrc_gpu_plan_create_band", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
+    "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
     "csrc_gpu_spmv_device_part", "csrc_gpu_set_timing", "csrc_gpu_last_timings",
@@ -164,4 +181,7 @@ EXPORTED = [
     "csrc_validate_coloring", "csrc_colorful_slices", "csrc_model_bytes", "csrc_model_flops",
     "csrc_fixture_generate", "csrc_fixture_matrix", "csrc_fixture_x", "csrc_fixture_order",
     "csrc_fixture_free", "csrc_fixture_u01",
+    "csrc_gpu_build_csr", "csrc_gpu_build_csrc", "csrc_gpu_csr_to_csrc", "csrc_gpu_decompose_rect",
+    "csrc_built_matrix", "csrc_built_csr", "csrc_built_rect_tail", "csrc_built_timings",
+    "csrc_built_free",
 ]

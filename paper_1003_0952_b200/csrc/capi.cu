@@ -153,7 +153,14 @@ struct csrc_gpu_plan_s {
     void* g_y = nullptr;
     cudaStream_t g_stream = nullptr;
 
+    // rectangular tail (CsrcRectMatrix, csrc_matrix.hpp:35-39): CSR over
+    // columns n..m-1, stored with global columns; x has m_cols entries
+    index_t m_cols = 0;  // 0: square plan
+    count_t rect_nnz = 0;
+    DevBuf rt_ptr, rt_col, rt_val;
+
     size_t vsize() const { return dtype == CSRC_DTYPE_F32 ? 4 : 8; }
+    index_t x_len() const { return m_cols ? m_cols : n_global; }
     index_t vec_len() const { return row_end - lo; }
     index_t x_hi = 0;  // gather: end of the x range the plan reads (band plans: above row_end)
     int launches = 0;
@@ -872,6 +879,11 @@ struct CreateOpts {
     int32_t bands = 0;
     bool band = false;
     index_t row_begin = 0, row_end = 0;
+    // rectangular tail (csrc_gpu_plan_create_rect)
+    int32_t m_cols = 0;
+    const int32_t* rect_ptr = nullptr;
+    const int32_t* rect_col = nullptr;
+    const double* rect_val = nullptr;
 };
 
 template <class T>
@@ -897,6 +909,15 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
         if (!a.value_symmetric) upload_values<T>(P.au, a.au + t0, static_cast<size_t>(P.k));
     }
     if (!colored) upload_values<T>(P.ad, a.ad + r0, static_cast<size_t>(P.nrows));
+    if (o.m_cols) {
+        P.m_cols = o.m_cols;
+        P.rect_nnz = o.rect_ptr[a.n];
+        std::vector<int32_t> gcol(static_cast<size_t>(P.rect_nnz));
+        for (count_t q = 0; q < P.rect_nnz; ++q) gcol[q] = a.n + o.rect_col[q];
+        upload(P.rt_ptr, o.rect_ptr, static_cast<size_t>(a.n) + 1);
+        upload(P.rt_col, gcol.data(), gcol.size());
+        upload_values<T>(P.rt_val, o.rect_val, static_cast<size_t>(P.rect_nnz));
+    }
     switch (P.exec_kind) {
         case CSRC_KIND_WINDOWED: {
             std::vector<index_t> bs;
@@ -976,6 +997,21 @@ Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const C
         for (index_t i = 0; i < a.n; ++i)
             if (o.color[i] < 0 || o.color[i] >= o.n_colors)
                 throw Error("coloring: row " + std::to_string(i) + " colour out of range");
+    }
+    if (o.m_cols) {
+        if (o.band) throw Error("band plans take square matrices only");
+        if (o.m_cols <= a.n)
+            throw Error("ParallelSpmv: rectangular matrix needs m > n (got m=" + std::to_string(o.m_cols) +
+                        ", n=" + std::to_string(a.n) + ")");
+        if (!o.rect_ptr || o.rect_ptr[0] != 0) throw Error("rect tail: row_ptr must start at 0");
+        for (index_t i = 0; i < a.n; ++i)
+            if (o.rect_ptr[i + 1] < o.rect_ptr[i]) throw Error("rect tail: row_ptr must be non-decreasing");
+        const count_t tn = o.rect_ptr[a.n];
+        if (tn > 0 && (!o.rect_col || !o.rect_val)) throw Error("rect tail: null column or value array");
+        for (count_t q = 0; q < tn; ++q)
+            if (o.rect_col[q] < 0 || o.rect_col[q] >= o.m_cols - a.n)
+                throw Error("rect tail: column " + std::to_string(o.rect_col[q]) + " outside [0, " +
+                            std::to_string(o.m_cols - a.n) + ")");
     }
     auto P = std::make_unique<Plan>();
     P->device = s->device;
@@ -1180,6 +1216,11 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
         default:
             throw Error("unknown strategy kind");
     }
+    if (P.m_cols) {
+        if (tr) throw Error("spmv_csrc_transpose: rectangular plans have no transpose product");
+        dev::k_rect_tail<T, 4><<<grid_for(P.device, P.nrows, 64), 256, 0, st>>>(
+            P.rt_ptr.as<int32_t>(), P.rt_col.as<int32_t>(), P.rt_val.as<T>(), x, y, P.nrows);
+    }
     rec(P, 3, st);
     P.ev_recorded = P.timing;
     CUDA_OK(cudaGetLastError());
@@ -1281,31 +1322,32 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
 }
 
 void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
-    if (x_len != P.n_global)
+    if (x_len != P.x_len())
         throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +
-                    std::to_string(P.n_global));
+                    std::to_string(P.x_len()));
     if (P.row_begin != 0 || P.row_end != P.n_global)
         throw Error("host products need a full-matrix plan (use the device entry points for bands)");
     if (P.n_global == 0) return;
     CUDA_OK(cudaSetDevice(P.device));
     const size_t n = static_cast<size_t>(P.n_global);
-    if (!P.dx.p) P.dx.alloc(n * P.vsize());
+    const size_t nx = static_cast<size_t>(P.x_len());
+    if (!P.dx.p) P.dx.alloc(nx * P.vsize());
     if (!P.dy.p) P.dy.alloc(n * P.vsize());
     cudaStream_t st = P.stream;
-    if (P.exec_kind == CSRC_KIND_GATHER && P.hchunk.size() > 2 && !P.timing) {
+    if (P.exec_kind == CSRC_KIND_GATHER && P.hchunk.size() > 2 && !P.timing && !P.m_cols) {
         apply_host_pipelined(P, xh, yh, tr);
         return;
     }
     if (P.dtype == CSRC_DTYPE_F64) {
-        CUDA_OK(cudaMemcpyAsync(P.dx.p, xh, n * 8, cudaMemcpyHostToDevice, st));
+        CUDA_OK(cudaMemcpyAsync(P.dx.p, xh, nx * 8, cudaMemcpyHostToDevice, st));
         apply_device(P, P.dx.p, P.dy.p, st, tr);
         CUDA_OK(cudaMemcpyAsync(yh, P.dy.p, n * 8, cudaMemcpyDeviceToHost, st));
     } else {
-        if (!P.dxd.p) P.dxd.alloc(n * 8);
+        if (!P.dxd.p) P.dxd.alloc(nx * 8);
         if (!P.dyd.p) P.dyd.alloc(n * 8);
-        CUDA_OK(cudaMemcpyAsync(P.dxd.p, xh, n * 8, cudaMemcpyHostToDevice, st));
-        dev::k_convert<double, float><<<grid_for(P.device, n, 256), 256, 0, st>>>(
-            P.dxd.as<double>(), P.dx.as<float>(), n);
+        CUDA_OK(cudaMemcpyAsync(P.dxd.p, xh, nx * 8, cudaMemcpyHostToDevice, st));
+        dev::k_convert<double, float><<<grid_for(P.device, nx, 256), 256, 0, st>>>(
+            P.dxd.as<double>(), P.dx.as<float>(), nx);
         apply_device(P, P.dx.p, P.dy.p, st, tr);
         dev::k_convert<float, double><<<grid_for(P.device, n, 256), 256, 0, st>>>(
             P.dy.as<float>(), P.dyd.as<double>(), n);
@@ -1349,6 +1391,22 @@ int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strat
         CreateOpts o;
         o.color = color;
         o.n_colors = n_colors;
+        *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_create_rect(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t m_cols,
+                              const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
+                              const double* tail_values, csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out) throw Error("null output");
+        *out = nullptr;
+        CreateOpts o;
+        o.m_cols = m_cols;
+        o.rect_ptr = tail_row_ptr;
+        o.rect_col = tail_col_idx;
+        o.rect_val = tail_values;
+        if (m_cols == 0) throw Error("ParallelSpmv: rectangular matrix needs m > n (got m=0)");
         *out = create_plan(a, s, o);
     });
 }
@@ -1409,7 +1467,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS
@@ -1439,6 +1497,17 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
                                                                          : gather_stage_smem<float>(P))
                                             : 0;
         }
+        info->m_cols = P.m_cols;
+        info->rect_nnz = P.rect_nnz;
+        if (P.m_cols) {
+            // tail: values + columns + row pointers, and the tail part of x (y RMW counted once)
+            const int64_t vs = static_cast<int64_t>(P.vsize());
+            info->model_bytes += P.rect_nnz * (vs + 4) + 4 * (static_cast<int64_t>(P.nrows) + 1) +
+                                 vs * (P.m_cols - P.n_global);
+            info->stream_bytes += P.rect_nnz * (vs + 4) + 4 * (static_cast<int64_t>(P.nrows) + 1) +
+                                  vs * (P.m_cols - P.n_global) + 2 * vs * P.nrows;
+            info->launches_per_apply += 1;
+        }
     });
 }
 
@@ -1450,6 +1519,7 @@ int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t 
                             double* y_host) {
     return guarded([&] {
         Plan& P = *checked(plan);
+        if (P.m_cols) throw Error("spmv_csrc_transpose: rectangular plans have no transpose product");
         if (x_len != P.n_global)
             throw Error("spmv_csrc_transpose: x has length " + std::to_string(x_len) +
                         ", expected " + std::to_string(P.n_global));

@@ -70,12 +70,8 @@ __global__ void __launch_bounds__(256) k_atomic(const int32_t* __restrict__ ia,
     }
 }
 
-// ----------------------------------------------------------------- gather
-// Transposed gather (CSRC_KIND_GATHER): the plan stores, per row q, the CSR
-// of the upper triangle (uptr/uidx = rows r with q in ja(r), uval = the
-// matching au values), so y_q = ad_q x_q + sum_lower al x[ja] + sum_upper
-// uval x[uidx] is a pure gather: every y element is written once, no
-// atomics, no zero-init, bit-reproducible.
+// The transposed-gather kernel (CSRC_KIND_GATHER) lives in gather.cuh.
+
 // ---------------------------------------------------------------- colored
 // One class per launch (colorful_worker, parallel.hpp:411-434): rows of a
 // class share no written y position, so y[j] += and y[i] += are plain
@@ -132,6 +128,33 @@ __global__ void k_convert(const Tin* __restrict__ in, Tout* __restrict__ out, in
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x)
         out[i] = static_cast<Tout>(in[i]);
+}
+
+// Rectangular tail (spmv_csrc_rect, kernels.hpp:84-86; ParallelSpmv
+// compute_block parallel.hpp:300-304): y[i] += sum_q tval[q] * x[tcol[q]]
+// over the CSR tail of row i, tcol already global (n + local column). L lanes
+// per row, shuffle reduction, one plain read-add-write of y[i] per row (the
+// square product has completed on the same stream).
+template <typename T, int L>
+__global__ void __launch_bounds__(256) k_rect_tail(const int32_t* __restrict__ tptr,
+                                                   const int32_t* __restrict__ tcol,
+                                                   const T* __restrict__ tval,
+                                                   const T* __restrict__ x, T* y, int32_t nrows) {
+    const int sub = threadIdx.x % L;
+    const int rows_per_block = blockDim.x / L;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * rows_per_block; base < nrows;
+         base += static_cast<int64_t>(gridDim.x) * rows_per_block) {
+        const int64_t r = base + threadIdx.x / L;
+        T s = T(0);
+        if (r < nrows) {
+            const int32_t q1 = __ldg(tptr + r + 1);
+            for (int32_t q = __ldg(tptr + r) + sub; q < q1; q += L)
+                s += ldg_stream(tval + q) * __ldg(x + ldg_stream(tcol + q));
+        }
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
+        if (r < nrows && sub == 0 && __ldg(tptr + r + 1) > __ldg(tptr + r)) y[r] += s;
+    }
 }
 
 template <typename T>

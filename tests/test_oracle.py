@@ -166,3 +166,31 @@ def test_oracle_matches_live_reference_on_fresh_matrices():
         a = P.CsrcMatrix(n, ref["ad"], ref["ia"], ref["ja"], ref["al"], ref["au"], ref["value_symmetric"])
         x = np.random.default_rng(i).uniform(-1, 1, n)
         assert np.array_equal(O.spmv_csrc(a, x), R.spmv_csrc(a, x))
+
+
+@pytest.mark.skipif(not Ref.available(), reason="reference shim oracle/_ref not built here")
+def test_oracle_rect_product_bit_exact():
+    """oracle_spmv_csrc_rect restates spmv_csrc_rect (kernels.hpp:69-91) in the
+    reference's FP order: bit-identical on the family plus random CSR tails."""
+    R = Ref()
+    rng = np.random.default_rng(3)
+    for idx in (0, 7, 19, 28):
+        a = FAM.matrix(f"m{idx}_")
+        extra = 11 + idx
+        cnt = rng.integers(0, 4, a.n)
+        rp = np.r_[0, np.cumsum(cnt)].astype(np.int32)
+        ci = np.concatenate([np.sort(rng.choice(extra, int(c), replace=False)) for c in cnt]).astype(np.int32)
+        r = P.CsrcRectMatrix(a, P.CsrMatrix(a.n, extra, rp, ci, rng.uniform(-1, 1, int(cnt.sum()))), a.n + extra)
+        x = rng.uniform(-1, 1, r.m)
+        assert np.array_equal(O.spmv_csrc_rect(r, x), R.spmv_csrc_rect(r, x))
+
+
+def test_csrc_to_triplets_order():
+    """P.csrc_to_triplets emits csrc_to_csr's triplet order (csrc_matrix.hpp:95-108)
+    and the oracle's build_csr -> csr_to_csrc inverts it bit for bit."""
+    a = MESH.matrix("g0_")
+    n, _, r, c, v = P.csrc_to_triplets(a)
+    assert r[0] == 0 and c[0] == 0 and v[0] == a.ad[0]
+    d = O.build_csrc(n, r, c, v)
+    for k in ("ad", "ia", "ja", "al", "au"):
+        assert np.array_equal(d[k], getattr(a, k))
