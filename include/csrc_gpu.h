@@ -240,6 +240,13 @@ int csrc_gpu_last_timings(csrc_gpu_plan_t plan, csrc_gpu_timings* t);
 int csrc_gpu_time_products(csrc_gpu_plan_t plan, const void* d_x, void* d_y, int32_t reps,
                            int64_t flush_bytes, double* ms_out, double* kernel_ms_out);
 
+/* Same, with x given on the host: x is uploaded once into the plan's own
+ * device vectors (converted to the plan's dtype), then `reps` device-resident
+ * products are timed. For harnesses without device memory of their own
+ * (the csrc_bench CLI). */
+int csrc_gpu_time_products_host(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, int32_t reps,
+                                int64_t flush_bytes, double* ms_out, double* kernel_ms_out);
+
 /* ------------------------------------------------- host plan builders
  * Product-side, scalable re-implementations of the reference's plan
  * functions; bit-exact with them (tests/test_plans.py). */

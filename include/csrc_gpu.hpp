@@ -98,15 +98,32 @@ csrc_host_matrix view(const M& a) {
     return m;
 }
 
+template <class P, class = void>
+struct has_square : std::false_type {};
+template <class P>
+struct has_square<P, std::void_t<decltype(std::declval<P>().square)>> : std::true_type {};
+
 /// GPU counterpart of csrc::ParallelSpmv (parallel.hpp:151-446). Unlike the
 /// reference it copies the matrix (device-resident), so `a` may be freed.
 class ParallelSpmv {
 public:
-    template <class M, class S>
+    template <class M, class S, std::enable_if_t<!has_square<M>::value, int> = 0>
     ParallelSpmv(const M& a, const S& s) : n_(a.n) {
         const csrc_host_matrix m = view(a);
         const csrc_gpu_strategy st = Strategy(s).c();
         check(csrc_gpu_plan_create(&m, &st, &plan_));
+    }
+
+    /// ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181):
+    /// any type with .square (CSRC), .rect (CSR tail, local columns) and .m.
+    template <class R, class S, std::enable_if_t<has_square<R>::value, int> = 0>
+    ParallelSpmv(const R& r, const S& s) : n_(r.square.n) {
+        const csrc_host_matrix m = view(r.square);
+        const csrc_gpu_strategy st = Strategy(s).c();
+        std::vector<int32_t> rp(r.rect.row_ptr.begin(), r.rect.row_ptr.end());
+        std::vector<int32_t> ci(r.rect.col_idx.begin(), r.rect.col_idx.end());
+        check(csrc_gpu_plan_create_rect(&m, &st, static_cast<int32_t>(r.m), rp.data(), ci.data(),
+                                        r.rect.values.data(), &plan_));
     }
 
     /// Explicit plan: a csrc::ColorfulPlan (has .coloring) or a
@@ -209,6 +226,166 @@ std::pair<Vector, PhaseTimings> spmv_parallel(const M& a, const Vector& x, const
     ParallelSpmv ex(a, s);
     Vector y = ex.apply(x);
     return {std::move(y), ex.last_timings()};
+}
+
+/// spmv_csrc_rect (kernels.hpp:69-91) on the GPU: x has r.m entries.
+template <class R>
+Vector spmv_csrc_rect(const R& r, const Vector& x) {
+    if (static_cast<long long>(x.size()) != static_cast<long long>(r.m))
+        throw Error("spmv_csrc_rect: x has length " + std::to_string(x.size()) + ", expected " +
+                    std::to_string(r.m));
+    ParallelSpmv ex(r, Strategy());
+    return ex.apply(x);
+}
+
+// ------------------------------------------------------------ construction
+// build_csr / csr_to_csrc / decompose_rect on the GPU (assemble.cu). The
+// results convert to the caller's own CsrMatrix / CsrcMatrix /
+// CsrcRectMatrix types (anything with the reference's member names), so
+//     csrc::CsrcMatrix c = csrc::gpu::csr_to_csrc(csrc::gpu::build_csr(t));
+// is a drop-in for csrc::csr_to_csrc(csrc::build_csr(t)) (csr.hpp:55-92,
+// csrc_matrix.hpp:44-91), bit-identical results.
+
+/// Canonical CSR (csrc::CsrMatrix shape, csr.hpp:28-51).
+struct CsrResult {
+    int32_t n_rows = 0, n_cols = 0;
+    std::vector<int32_t> row_ptr, col_idx;
+    std::vector<double> values;
+    template <class C>
+    operator C() const {  // NOLINT(google-explicit-constructor): drop-in
+        C c;
+        c.n_rows = n_rows;
+        c.n_cols = n_cols;
+        c.row_ptr.assign(row_ptr.begin(), row_ptr.end());
+        c.col_idx.assign(col_idx.begin(), col_idx.end());
+        c.values.assign(values.begin(), values.end());
+        return c;
+    }
+};
+
+/// CSRC (csrc::CsrcMatrix shape, csrc_matrix.hpp:14-30).
+struct CsrcResult {
+    int32_t n = 0;
+    std::vector<double> ad;
+    std::vector<int32_t> ia, ja;
+    std::vector<double> al, au;
+    bool value_symmetric = false;
+    template <class C>
+    operator C() const {  // NOLINT(google-explicit-constructor): drop-in
+        C c;
+        c.n = n;
+        c.ad.assign(ad.begin(), ad.end());
+        c.ia.assign(ia.begin(), ia.end());
+        c.ja.assign(ja.begin(), ja.end());
+        c.al.assign(al.begin(), al.end());
+        c.au.assign(au.begin(), au.end());
+        c.value_symmetric = value_symmetric;
+        return c;
+    }
+};
+
+/// csrc::CsrcRectMatrix shape (csrc_matrix.hpp:35-39).
+struct CsrcRectResult {
+    CsrcResult square;
+    CsrResult rect;
+    int32_t m = 0;
+    template <class C>
+    operator C() const {  // NOLINT(google-explicit-constructor): drop-in
+        C c;
+        c.square = square;
+        c.rect = rect;
+        c.m = m;
+        return c;
+    }
+};
+
+namespace detail {
+struct Built {
+    csrc_built_t h = nullptr;
+    ~Built() { csrc_built_free(h); }
+};
+inline CsrcResult take_csrc(csrc_built_t h) {
+    csrc_host_matrix m;
+    check(csrc_built_matrix(h, &m));
+    CsrcResult c;
+    c.n = m.n;
+    c.ad.assign(m.ad, m.ad + m.n);
+    c.ia.assign(m.ia, m.ia + m.n + 1);
+    c.ja.assign(m.ja, m.ja + m.k);
+    c.al.assign(m.al, m.al + m.k);
+    if (!m.value_symmetric) c.au.assign(m.au, m.au + m.k);
+    c.value_symmetric = m.value_symmetric != 0;
+    return c;
+}
+template <class M>
+void csr_arrays(const M& a, std::vector<int32_t>& rp, std::vector<int32_t>& ci) {
+    rp.assign(a.row_ptr.begin(), a.row_ptr.end());
+    ci.assign(a.col_idx.begin(), a.col_idx.end());
+}
+}  // namespace detail
+
+/// build_csr (csr.hpp:55-92): t is a csrc::TripletMatrix (n_rows, n_cols,
+/// entries {row, col, value}). Duplicates summed in input order.
+template <class T>
+CsrResult build_csr(const T& t, int device = 0) {
+    std::vector<int32_t> r, c;
+    std::vector<double> v;
+    r.reserve(t.entries.size());
+    c.reserve(t.entries.size());
+    v.reserve(t.entries.size());
+    for (const auto& e : t.entries) {
+        r.push_back(e.row);
+        c.push_back(e.col);
+        v.push_back(e.value);
+    }
+    detail::Built b;
+    check(csrc_gpu_build_csr(t.n_rows, t.n_cols, static_cast<int64_t>(v.size()), r.data(), c.data(), v.data(),
+                             device, &b.h));
+    int32_t nr = 0, nc = 0;
+    int64_t nnz = 0;
+    const int32_t *rp = nullptr, *ci = nullptr;
+    const double* va = nullptr;
+    check(csrc_built_csr(b.h, &nr, &nc, &nnz, &rp, &ci, &va));
+    CsrResult out;
+    out.n_rows = nr;
+    out.n_cols = nc;
+    out.row_ptr.assign(rp, rp + nr + 1);
+    out.col_idx.assign(ci, ci + nnz);
+    out.values.assign(va, va + nnz);
+    return out;
+}
+
+/// csr_to_csrc (csrc_matrix.hpp:44-91) of a canonical CSR.
+template <class M>
+CsrcResult csr_to_csrc(const M& a, int device = 0) {
+    std::vector<int32_t> rp, ci;
+    detail::csr_arrays(a, rp, ci);
+    detail::Built b;
+    check(csrc_gpu_csr_to_csrc(a.n_rows, a.n_cols, rp.data(), ci.data(), a.values.data(), device, &b.h));
+    return detail::take_csrc(b.h);
+}
+
+/// decompose_rect (csrc_matrix.hpp:113-142, symmetrize = false).
+template <class M>
+CsrcRectResult decompose_rect(const M& a, int device = 0) {
+    std::vector<int32_t> rp, ci;
+    detail::csr_arrays(a, rp, ci);
+    detail::Built b;
+    check(csrc_gpu_decompose_rect(a.n_rows, a.n_cols, rp.data(), ci.data(), a.values.data(), device, &b.h));
+    CsrcRectResult r;
+    r.square = detail::take_csrc(b.h);
+    int32_t m = 0;
+    int64_t nnz = 0;
+    const int32_t *trp = nullptr, *tci = nullptr;
+    const double* tva = nullptr;
+    check(csrc_built_rect_tail(b.h, &m, &nnz, &trp, &tci, &tva));
+    r.m = m;
+    r.rect.n_rows = r.square.n;
+    r.rect.n_cols = m - r.square.n;
+    r.rect.row_ptr.assign(trp, trp + r.square.n + 1);
+    r.rect.col_idx.assign(tci, tci + nnz);
+    r.rect.values.assign(tva, tva + nnz);
+    return r;
 }
 
 }  // namespace gpu

@@ -133,6 +133,7 @@ band_split = _sig("csrc_gpu_band_split", C.c_int, vp, P_i32)
 set_timing = _sig("csrc_gpu_set_timing", C.c_int, vp, i32)
 last_timings = _sig("csrc_gpu_last_timings", C.c_int, vp, C.POINTER(Timings))
 time_products = _sig("csrc_gpu_time_products", C.c_int, vp, vp, vp, i32, i64, P_f64, P_f64)
+time_products_host = _sig("csrc_gpu_time_products_host", C.c_int, vp, P_f64, i64, i32, i64, P_f64, P_f64)
 
 partition_by_nnz = _sig("csrc_partition_by_nnz", C.c_int, PM, i32, P_i32, P_i64)
 effective_ranges = _sig("csrc_effective_ranges", C.c_int, PM, i32, P_i32, P_i32, P_i32)
@@ -176,7 +177,7 @@ EXPORTED = [
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
     "csrc_gpu_spmv_device_part", "csrc_gpu_set_timing", "csrc_gpu_last_timings",
-    "csrc_gpu_time_products", "csrc_partition_by_nnz", "csrc_effective_ranges",
+    "csrc_gpu_time_products", "csrc_gpu_time_products_host", "csrc_partition_by_nnz", "csrc_effective_ranges",
     "csrc_interval_plan", "csrc_color_rows", "csrc_conflict_edge_counts",
     "csrc_validate_coloring", "csrc_colorful_slices", "csrc_model_bytes", "csrc_model_flops",
     "csrc_fixture_generate", "csrc_fixture_matrix", "csrc_fixture_x", "csrc_fixture_order",

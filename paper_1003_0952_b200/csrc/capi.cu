@@ -121,6 +121,14 @@ struct csrc_gpu_plan_s {
     int32_t n_patterns = 0;
     DevBuf pbase, pat_off;
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
+    // sliced form (k_gather_sell, default): SELL-32 layout of the entry stream
+    int gather_sell = 0;
+    int sell_u = 8;        // entries in flight per thread
+    int sell_lanes = 1;    // lanes per row (slice height 32 / lanes)
+    int sell_grid = 0;
+    int64_t sell_entries = 0;  // padded entries (32 x sum of slice widths)
+    int sell_pat_len = 0;      // offset-table entries staged in shared memory
+    DevBuf sbase, rmeta, sidx, sval, sval_t;
     int gather_grid = 0;
     // host-API pipeline (apply_host): row chunks, and for each the last x chunk it reads
     std::vector<int32_t> hchunk;
@@ -674,6 +682,94 @@ void* gather_stage_fn(const Plan& P) {
     }
 }
 
+template <class T, int L, bool PAT>
+void* sell_fn_LP(int u) {
+    switch (u) {
+        case 4: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 4>);
+        case 12: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 12>);
+        default: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 8>);
+    }
+}
+
+template <class T>
+void* sell_fn(const Plan& P) {
+    const bool pat = P.gather_pat != 0;
+    switch (P.sell_lanes) {
+        case 2: return pat ? sell_fn_LP<T, 2, true>(P.sell_u) : sell_fn_LP<T, 2, false>(P.sell_u);
+        case 4: return pat ? sell_fn_LP<T, 4, true>(P.sell_u) : sell_fn_LP<T, 4, false>(P.sell_u);
+        default: return pat ? sell_fn_LP<T, 1, true>(P.sell_u) : sell_fn_LP<T, 1, false>(P.sell_u);
+    }
+}
+
+// Sliced layout of the entry stream (gather.cuh k_gather_sell): slice s =
+// rows [H s, H s + H), H = 32 / L; width = ceil(longest row / L) steps of 32
+// slots; entry j of local row rl at sbase[s] + 32 (j / L) + L rl + j % L;
+// padding slots hold zeros and are never read.
+template <class T>
+void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const std::vector<int32_t>& eidx,
+                const std::vector<double>& ev, const std::vector<double>& evt, bool value_symmetric,
+                const std::vector<int32_t>& pbase, const std::vector<int32_t>& pat_off) {
+    const double avg = n ? static_cast<double>(eptr[n]) / n : 0.0;
+    // lanes per row: rows of <= 40 entries (27-point stencils) split over 2
+    // lanes, longer rows (81-entry elasticity) one lane (profiles/r01_sweep_sell*.txt)
+    const int L = env_int("CSRC_GPU_SELL_L", avg <= 40 ? 2 : 1);
+    P.sell_lanes = (L == 2 || L == 4) ? L : 1;
+    const int H = 32 / P.sell_lanes;
+    const int64_t ns = (static_cast<int64_t>(n) + H - 1) / H;
+    std::vector<int32_t> sbase(static_cast<size_t>(ns) + 1, 0);
+    int32_t maxlen = 0;
+    for (int64_t sl = 0; sl < ns; ++sl) {
+        int32_t w = 0;
+        for (int64_t r = sl * H; r < std::min<int64_t>(n, sl * H + H); ++r) w = std::max(w, eptr[r + 1] - eptr[r]);
+        maxlen = std::max(maxlen, w);
+        const int64_t steps = (w + P.sell_lanes - 1) / P.sell_lanes;
+        const int64_t next = static_cast<int64_t>(sbase[sl]) + 32 * steps;
+        if (next > INT32_MAX) throw Error("gather plan: padded slice layout exceeds 2^31 entries");
+        sbase[sl + 1] = static_cast<int32_t>(next);
+    }
+    // pattern form: offset table in shared memory (<= 16 K entries), rows < 2^11 entries
+    const bool pat = P.gather_pat && maxlen < 2048 && pat_off.size() <= (size_t(1) << 14);
+    P.gather_pat = pat ? 1 : 0;
+    const size_t tot = static_cast<size_t>(sbase[ns]);
+    P.sell_entries = static_cast<int64_t>(tot);
+    std::vector<int32_t> rmeta(static_cast<size_t>(n));
+    std::vector<int32_t> sidx(pat ? 0 : tot, 0);
+    std::vector<double> sv(tot, 0.0), svt(value_symmetric ? 0 : tot, 0.0);
+    const int Ln = P.sell_lanes;
+    for (int64_t sl = 0; sl < ns; ++sl)
+        for (int64_t r = sl * H; r < std::min<int64_t>(n, sl * H + H); ++r) {
+            const int32_t len = eptr[r + 1] - eptr[r];
+            rmeta[r] = pat ? (pbase[r] | (len << 20)) : len;
+            const size_t b = static_cast<size_t>(sbase[sl]) + static_cast<size_t>(Ln * (r - sl * H));
+            for (int32_t j = 0; j < len; ++j) {
+                const size_t d = b + 32 * static_cast<size_t>(j / Ln) + static_cast<size_t>(j % Ln);
+                sv[d] = ev[eptr[r] + j];
+                if (!value_symmetric) svt[d] = evt[eptr[r] + j];
+                if (!pat) sidx[d] = eidx[eptr[r] + j];
+            }
+        }
+    upload(P.sbase, sbase.data(), sbase.size());
+    upload(P.rmeta, rmeta.data(), rmeta.size());
+    upload_values<T>(P.sval, sv.data(), sv.size());
+    if (!value_symmetric) upload_values<T>(P.sval_t, svt.data(), svt.size());
+    if (pat) upload(P.pat_off, pat_off.data(), pat_off.size());
+    else upload(P.sidx, sidx.data(), sidx.size());
+    if (!pat) P.n_patterns = 0;
+    const int u = env_int("CSRC_GPU_SELL_U", 8);
+    P.sell_u = (u == 4 || u == 12) ? u : 8;
+    P.gather_sell = 1;
+    P.gather_buf = 0;
+    P.sell_pat_len = pat ? static_cast<int>(pat_off.size()) : 0;
+    void* fn = sell_fn<T>(P);
+    const int smem = 4 * P.sell_pat_len;
+    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+    const int64_t blocks = (ns + 7) / 8;
+    P.sell_grid = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(blocks, static_cast<int64_t>(num_sms(P.device)) * std::max(occ, 1))));
+}
+
 template <class T>
 void setup_gather(Plan& P, const MatView& a) {
     // rows [r0, r1) of the global matrix (the whole matrix unless a band plan);
@@ -797,6 +893,10 @@ void setup_gather(Plan& P, const MatView& a) {
             }
         }
     }
+    if (env_int("CSRC_GPU_GSELL", 1) != 0 && n > 0) {
+        setup_sell<T>(P, n, eptr, eidx, ev, evt, a.value_symmetric, pbase, pat_off);
+        return;
+    }
     if (!P.gather_buf) P.gather_pat = 0;  // the plain row kernel reads explicit indices
     if (P.gather_pat) {
         upload(P.pbase, pbase.data(), pbase.size());
@@ -834,6 +934,28 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
                          cudaStream_t st) {
     if (r1 <= r0) return;
     x += P.row_begin - P.lo;  // band plans: x holds [lo, x_hi), columns are band-row relative
+    if (P.gather_sell) {
+        dev::GSellArgs<T> A;
+        A.sbase = P.sbase.as<int32_t>();
+        A.rmeta = P.rmeta.as<int32_t>();
+        A.sidx = P.sidx.as<int32_t>();
+        A.pat_off = P.pat_off.as<int32_t>();
+        A.sval = (tr && !P.value_symmetric ? P.sval_t : P.sval).template as<T>();
+        A.ad = P.ad.as<T>();
+        A.x = x;
+        A.y = y;
+        const int H = 32 / P.sell_lanes;
+        A.slice0 = r0 / H;
+        A.slice1 = (r1 + H - 1) / H;
+        A.nrows = r1;
+        A.pat_len = P.sell_pat_len;
+        const int64_t blocks = (static_cast<int64_t>(A.slice1 - A.slice0) + 7) / 8;
+        const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, P.sell_grid)));
+        void* args[] = {&A};
+        CUDA_OK(cudaLaunchKernel(sell_fn<T>(P), dim3(grid), dim3(256), args, static_cast<size_t>(4 * P.sell_pat_len),
+                                 st));
+        return;
+    }
     const T* vals = (tr && !P.value_symmetric ? P.eval_t : P.eval).template as<T>();
     if (P.gather_buf) {
         const int R = P.gather_nt / P.gather_lanes;
@@ -1467,7 +1589,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS
@@ -1490,8 +1612,15 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
             // entry values + (indices | per-row pattern start) + eptr + ad, x, y
             info->stream_bytes = ne * vs + (P.gather_pat ? 4 * static_cast<int64_t>(P.nrows) : 4 * ne) +
                                  4 * (static_cast<int64_t>(P.nrows) + 1) + 3 * vs * P.nrows;
+            if (P.gather_sell) {
+                // padded slice values (+ columns) + rmeta + slice bases + ad, x, y
+                const int64_t pe = P.sell_entries;
+                const int64_t H = 32 / P.sell_lanes;
+                info->stream_bytes = pe * vs + (P.gather_pat ? 0 : 4 * pe) + 4 * static_cast<int64_t>(P.nrows) +
+                                     4 * ((static_cast<int64_t>(P.nrows) + H - 1) / H + 1) + 3 * vs * P.nrows;
+            }
             info->row_patterns = P.gather_pat ? P.n_patterns : 0;
-            info->lanes = P.gather_lanes;
+            info->lanes = P.gather_sell ? P.sell_lanes : P.gather_lanes;
             info->stages = P.gather_buf ? P.gather_nb : 0;
             info->smem_bytes = P.gather_buf ? (P.dtype == CSRC_DTYPE_F64 ? gather_stage_smem<double>(P)
                                                                          : gather_stage_smem<float>(P))
@@ -1654,6 +1783,31 @@ int csrc_gpu_time_products(csrc_gpu_plan_t plan, const void* d_x, void* d_y, int
             throw;
         }
         P.timing = was;
+    });
+}
+
+int csrc_gpu_time_products_host(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, int32_t reps,
+                                int64_t flush_bytes, double* ms_out, double* kernel_ms_out) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (x_len != P.x_len())
+            throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +
+                        std::to_string(P.x_len()));
+        if (P.row_begin != 0 || P.row_end != P.n_global)
+            throw Error("host products need a full-matrix plan (use the device entry points for bands)");
+        if (P.n_global == 0) return;
+        CUDA_OK(cudaSetDevice(P.device));
+        const size_t nx = static_cast<size_t>(P.x_len());
+        if (!P.dx.p) P.dx.alloc(nx * P.vsize());
+        if (!P.dy.p) P.dy.alloc(static_cast<size_t>(P.n_global) * P.vsize());
+        if (P.dtype == CSRC_DTYPE_F64) {
+            CUDA_OK(cudaMemcpy(P.dx.p, x_host, nx * 8, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<float> xf(x_host, x_host + nx);
+            CUDA_OK(cudaMemcpy(P.dx.p, xf.data(), nx * 4, cudaMemcpyHostToDevice));
+        }
+        if (csrc_gpu_time_products(plan, P.dx.p, P.dy.p, reps, flush_bytes, ms_out, kernel_ms_out) != 0)
+            throw Error(csrc_gpu_last_error());
     });
 }
 

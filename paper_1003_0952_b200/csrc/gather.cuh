@@ -236,5 +236,140 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     }
 }
 
+// Ordered read-only loads: volatile asm keeps the issue order of a batch of
+// independent loads (ptxas otherwise interleaves each gather with its FMA and
+// keeps only ~2 loads in flight per thread in the pattern form).
+__device__ __forceinline__ double ld_nc(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_nc(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_nc(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_cs(const double* p) {
+    double v;
+    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_cs(const float* p) {
+    float v;
+    asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_cs(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Sliced form (k_gather_sell, the default for mesh matrices): the entry
+// stream re-laid out in slices of H = 32 / L consecutive rows, one warp per
+// slice, L lanes per row. Entry j of the slice's local row rl sits at
+//     sbase[s] + 32 (j / L) + L rl + (j % L)
+// (SELL-H with L-way interleave; rows shorter than the slice's longest are
+// padded, the padding never read), so every value load of a warp is one
+// contiguous 32 x sizeof(T) segment, and in the row-pattern form the x gather
+// of step t is one contiguous run too (H consecutive rows, same stencil
+// offsets). Each lane issues the U value and U x loads of its next U entries
+// back to back from registers: no shared-memory staging, no block barriers,
+// no TMA round trip per row block -- bytes in flight per SM are set by
+// registers (U x 2 x sizeof(T) per thread), not by a staged buffer held for a
+// whole compute phase (k_gather_staged). Values and columns are read once:
+// evict-first (ld.global.cs).
+//   rmeta[row]: PAT: pattern start | len << 20 (offset table <= 2^14 entries,
+//               held in shared memory; len < 2^11); explicit: len, columns in sidx.
+// Summation order per row: lane sub takes entries j = sub + L t, even t into
+// acc0, odd t into acc1; acc0 + acc1; xor-shuffle over the L lanes; + ad x.
+// Identical in both forms and for every launch split (host pipeline chunks).
+template <typename T>
+struct GSellArgs {
+    const int32_t* sbase;    // [n_slices + 1] entry offset of each slice
+    const int32_t* rmeta;    // [nrows]
+    const int32_t* sidx;     // !PAT: columns, slice layout
+    const int32_t* pat_off;  // PAT
+    const T* sval;           // values, slice layout
+    const T* ad;
+    const T* x;
+    T* y;
+    int32_t slice0, slice1;  // slices [slice0, slice1)
+    int32_t nrows;           // rows >= nrows are skipped (last slice)
+    int32_t pat_len;         // PAT: table entries copied to shared memory
+};
+
+// resident 256-thread blocks per SM the register budget is sized for
+template <int U> struct SellMinBlocks { static constexpr int value = U <= 4 ? 4 : U <= 8 ? 3 : 2; };
+
+template <typename T, int L, bool PAT, int U>
+__global__ void __launch_bounds__(256, SellMinBlocks<U>::value) k_gather_sell(const GSellArgs<T> A) {
+    static_assert(L == 1 || L == 2 || L == 4, "lanes per row");
+    constexpr int H = 32 / L;
+    // PAT: the offset table (a few KB for mesh stencils) lives in shared memory,
+    // so each x gather waits on a ~30-cycle LDS instead of an L1 round trip
+    extern __shared__ __align__(16) int32_t s_pat[];
+    if (PAT) {
+        for (int i = threadIdx.x; i < A.pat_len; i += blockDim.x) s_pat[i] = __ldg(A.pat_off + i);
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % L;
+    const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t s = A.slice0 + ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+         s < A.slice1; s += nwarps) {  // warp-uniform: the shuffles below see all 32 lanes
+        const int32_t row = static_cast<int32_t>(s * H + lane / L);
+        const bool act = row < A.nrows;
+        int32_t nt = 0, pb = 0;
+        if (act) {
+            const int32_t meta = __ldg(A.rmeta + row);
+            const int32_t len = PAT ? (meta >> 20) : meta;
+            pb = PAT ? (meta & 0xFFFFF) + sub : 0;
+            nt = len > sub ? (len - sub + L - 1) / L : 0;  // this lane's entries
+        }
+        const int64_t base = static_cast<int64_t>(__ldg(A.sbase + s)) + lane;
+        const T* vp = A.sval + base;
+        const int32_t* ip = A.sidx + base;
+        T acc0 = T(0), acc1 = T(0);
+        // U steps at a time: U offset/column loads, U value loads, U x gathers,
+        // each batch predicated on t < nt, then the FMAs in step order. (The
+        // predication also keeps ptxas from pairing each gather with its FMA,
+        // which makes the in-order warp stall on every load in turn.)
+#pragma unroll 1
+        for (int32_t t0 = 0; t0 < nt; t0 += U) {
+            T v[U], xv[U];
+            int32_t c[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (t0 + u < nt)
+                    c[u] = PAT ? row + s_pat[pb + L * (t0 + u)] : ld_cs(ip + 32 * static_cast<int64_t>(t0 + u));
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (t0 + u < nt) v[u] = ld_cs(vp + 32 * static_cast<int64_t>(t0 + u));
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (t0 + u < nt) xv[u] = ld_nc(A.x + c[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (t0 + u < nt) {
+                    if (u & 1)
+                        acc1 = fma(v[u], xv[u], acc1);
+                    else
+                        acc0 = fma(v[u], xv[u], acc0);
+                }
+            }
+        }
+        T sum = acc0 + acc1;
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, L);
+        if (act && sub == 0) A.y[row] = sum + __ldg(A.ad + row) * __ldg(A.x + row);
+    }
+}
+
 }  // namespace dev
 }  // namespace csrcgpu

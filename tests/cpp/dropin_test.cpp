@@ -46,6 +46,41 @@ int main() {
         auto [y, t] = gpu::spmv_parallel(c, x, Strategy{StrategyKind::colorful, AccumMethod::effective, 2});
         worst = std::max(worst, max_rel(y, ref));
     }
+    // construction on the GPU: bit-identical CSR and CSRC, reference types out
+    for (int i = 0; i < 6; ++i) {
+        TripletMatrix t = generate_random_sym(60 + 31 * i, 0.06, 99 + i, i % 2 == 0);
+        CsrMatrix ref_csr = build_csr(t);
+        CsrMatrix got_csr = gpu::build_csr(t);
+        if (got_csr.row_ptr != ref_csr.row_ptr || got_csr.col_idx != ref_csr.col_idx ||
+            got_csr.values != ref_csr.values)
+            ++fails;
+        CsrcMatrix ref_c = csr_to_csrc(ref_csr);
+        CsrcMatrix got_c = gpu::csr_to_csrc(gpu::build_csr(t));
+        if (got_c.ia != ref_c.ia || got_c.ja != ref_c.ja || got_c.ad != ref_c.ad || got_c.al != ref_c.al ||
+            got_c.au != ref_c.au || got_c.value_symmetric != ref_c.value_symmetric)
+            ++fails;
+    }
+    // rectangular products: decompose_rect + spmv_csrc_rect / ParallelSpmv(rect, s)
+    {
+        const index_t n = 120, extra = 17;
+        TripletMatrix sq = generate_random_sym(n, 0.05, 7);
+        TripletMatrix t;
+        t.n_rows = n;
+        t.n_cols = n + extra;
+        t.entries = sq.entries;
+        for (index_t i = 0; i < n; i += 3) t.add(i, n + (i % extra), 0.25 * (1 + i % 5));
+        CsrMatrix full = build_csr(t);
+        CsrcRectMatrix ref_r = decompose_rect(full);
+        CsrcRectMatrix got_r = gpu::decompose_rect(full);
+        if (got_r.m != ref_r.m || got_r.square.ja != ref_r.square.ja || got_r.square.al != ref_r.square.al ||
+            got_r.rect.col_idx != ref_r.rect.col_idx || got_r.rect.values != ref_r.rect.values)
+            ++fails;
+        Vector x = bench_source_vector(n + extra);
+        Vector ref = spmv_csrc_rect(ref_r, x);
+        worst = std::max(worst, max_rel(gpu::spmv_csrc_rect(got_r, x), ref));
+        gpu::ParallelSpmv ex(ref_r, Strategy{StrategyKind::local_buffers, AccumMethod::interval, 4});
+        worst = std::max(worst, max_rel(ex.apply(x), ref));
+    }
     // error behaviour: the reference's csrc::Error with its wording
     try {
         CsrcMatrix c = csr_to_csrc(build_csr(generate_band(10, 1)));
