@@ -253,6 +253,8 @@ def main():
         kms = float(np.mean(ker))
         info = ex.info()
         layout_bytes, row_patterns = int(info.stream_bytes), int(info.row_patterns)
+        kernel_name = {1: "k_gather_rows", 2: "k_gather_staged", 3: "k_gather_sell"}.get(
+            int(info.gather_form), {"windowed": "k_windowed", "atomic": "k_atomic"}.get(args.kind, args.kind))
         # our kernels per product (the y memset of windowed/atomic is a driver memset, not counted)
         launches_per_step = 1 if args.kind in ("gather", "windowed", "atomic") else info.launches_per_apply
         others = {}
@@ -285,6 +287,7 @@ def main():
     else:
         others = {}
         layout_bytes, row_patterns = None, 0
+        kernel_name = "k_gather_staged" if args.kind == "gather" else "k_" + args.kind
         from paper_1003_0952_b200.dist import DistSpmv
         ds = DistSpmv(a, strat)
         p = ds.plan
@@ -347,8 +350,7 @@ def main():
         gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
         roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
                       traffic=load_traffic(wl), peak_source=peak_src,
-                      kernel={"gather": "k_gather_staged", "windowed": "k_windowed", "atomic": "k_atomic"}.get(
-                          args.kind, args.kind),
+                      kernel=kernel_name,
                       algorithmic_bytes_per_launch=mb, kernel_ms=kms,
                       layout_bytes_per_launch=layout_bytes,
                       layout_frac=(layout_bytes / (kms / 1e3) / 1e9) / peak if layout_bytes else None,

@@ -139,6 +139,8 @@ typedef struct {
                                    gather band plans also read x above the band       */
     int32_t m_cols;             /* rectangular plans: columns of A (x length); 0 = square */
     int64_t rect_nnz;           /* rectangular plans: entries of the CSR tail        */
+    int32_t gather_form;        /* gather plans: 1 k_gather_rows, 2 k_gather_staged,
+                                   3 k_gather_sell; 0 for the other kinds            */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;

@@ -85,6 +85,7 @@ class PlanInfo(C.Structure):
         ("x_hi", i32),
         ("m_cols", i32),
         ("rect_nnz", i64),
+        ("gather_form", i32),
     ]
 
 

@@ -121,6 +121,10 @@ struct csrc_gpu_plan_s {
     int32_t n_patterns = 0;
     DevBuf pbase, pat_off;
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
+    // staged-x pattern form (k_gather_staged PF = 2)
+    int gather_xs = 0;
+    int xs_clusters = 0, xs_tab_len = 0, xs_bytes = 0;
+    DevBuf xs_tab, xs_clo, xs_chi, xs_cbase;
     // sliced form (k_gather_sell, default): SELL-32 layout of the entry stream
     int gather_sell = 0;
     int sell_u = 8;        // entries in flight per thread
@@ -654,39 +658,102 @@ bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const std::v
 template <class T>
 int gather_stage_smem(const Plan& P) {
     return 16 + P.gather_nb * ((P.gather_pat ? 0 : dev::gather_idx_bytes(P.gather_cap)) +
-                               dev::gather_val_bytes<T>(P.gather_cap));
+                               dev::gather_val_bytes<T>(P.gather_cap) + (P.gather_xs ? P.xs_bytes : 0));
+}
+
+// pattern form of the staged kernel: 0 explicit columns, 1 row patterns, 2 patterns + staged x
+int gather_pf(const Plan& P) { return P.gather_pat ? (P.gather_xs ? 2 : 1) : 0; }
+
+template <class T, int L, int U, int NB, int MINB>
+void* gather_stage_fn_M(int pf) {
+    switch (pf) {
+        case 2: return reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, 2, MINB>);
+        case 1: return reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, 1, MINB>);
+        default: return reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, 0, MINB>);
+    }
 }
 
 template <class T, int L, int U, int NB>
-void* gather_stage_fn_NB(bool pat, int minb) {
-    if (minb == 8)
-        return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true, 8>)
-                   : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false, 8>);
-    return pat ? reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, true, 1>)
-               : reinterpret_cast<void*>(&dev::k_gather_staged<T, L, U, NB, false, 1>);
+void* gather_stage_fn_NB(int pf, int minb) {
+    return minb == 8 ? gather_stage_fn_M<T, L, U, NB, 8>(pf) : gather_stage_fn_M<T, L, U, NB, 1>(pf);
 }
 
 template <class T, int L>
-void* gather_stage_fn_L(int U, int NB, bool pat, int minb) {
+void* gather_stage_fn_L(int U, int NB, int pf, int minb) {
     if (U == 8)
-        return NB == 2 ? gather_stage_fn_NB<T, L, 8, 2>(pat, minb) : gather_stage_fn_NB<T, L, 8, 1>(pat, minb);
-    return NB == 2 ? gather_stage_fn_NB<T, L, 4, 2>(pat, minb) : gather_stage_fn_NB<T, L, 4, 1>(pat, minb);
+        return NB == 2 ? gather_stage_fn_NB<T, L, 8, 2>(pf, minb) : gather_stage_fn_NB<T, L, 8, 1>(pf, minb);
+    return NB == 2 ? gather_stage_fn_NB<T, L, 4, 2>(pf, minb) : gather_stage_fn_NB<T, L, 4, 1>(pf, minb);
 }
 
 template <class T>
 void* gather_stage_fn(const Plan& P) {
+    const int pf = gather_pf(P);
     switch (P.gather_lanes) {
-        case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
-        case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
-        default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, P.gather_pat, P.gather_minb);
+        case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, pf, P.gather_minb);
+        case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, pf, P.gather_minb);
+        default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, pf, P.gather_minb);
     }
+}
+
+// Staged-x form (k_gather_staged, PF = 2): the pattern dictionary's column
+// offsets grouped into clusters (a new cluster after a gap of more than 32);
+// row block [q0, q0 + R) reads x only on [q0 + clo_k, q0 + R + chi_k), copied
+// by TMA next to the values. Per alignment phase ph of the x pointer
+// (16-byte grain), xs_tab[ph][i] = cbase_k + ((ph + clo_k) mod m) + (d_i - clo_k)
+// locates pattern entry i's x value relative to the row's local index.
+// Returns false (staged x off) past 32 clusters or 24 KB of x per row block.
+template <class T>
+bool setup_staged_x(Plan& P, const std::vector<int32_t>& pat_off) {
+    const int R = P.gather_nt / P.gather_lanes;
+    const int m = 16 / static_cast<int>(sizeof(T));
+    std::vector<int32_t> offs(pat_off.begin(), pat_off.end());
+    std::sort(offs.begin(), offs.end());
+    offs.erase(std::unique(offs.begin(), offs.end()), offs.end());
+    if (offs.empty()) return false;
+    std::vector<int32_t> clo, chi, cbase;
+    for (size_t i = 0; i < offs.size(); ++i) {
+        if (clo.empty() || static_cast<int64_t>(offs[i]) - chi.back() > 32) {
+            clo.push_back(offs[i]);
+            chi.push_back(offs[i]);
+        } else {
+            chi.back() = offs[i];
+        }
+    }
+    if (clo.size() > 32) return false;
+    int64_t acc = 0;
+    for (size_t k = 0; k < clo.size(); ++k) {
+        cbase.push_back(static_cast<int32_t>(acc));
+        const int64_t cap = R + (static_cast<int64_t>(chi[k]) - clo[k]) + 2 * m;
+        acc += (cap + m - 1) / m * m;
+    }
+    const int64_t bytes = acc * static_cast<int64_t>(sizeof(T));
+    if (bytes > 24 * 1024) return false;
+    const size_t tl = pat_off.size();
+    std::vector<int32_t> tab(tl * m);
+    for (int ph = 0; ph < m; ++ph)
+        for (size_t i = 0; i < tl; ++i) {
+            const int32_t d = pat_off[i];
+            const size_t k = static_cast<size_t>(std::upper_bound(clo.begin(), clo.end(), d) - clo.begin()) - 1;
+            const int32_t pad = static_cast<int32_t>(((ph + static_cast<int64_t>(clo[k])) % m + m) % m);
+            tab[ph * tl + i] = cbase[k] + pad + (d - clo[k]);
+        }
+    upload(P.xs_tab, tab.data(), tab.size());
+    upload(P.xs_clo, clo.data(), clo.size());
+    upload(P.xs_chi, chi.data(), chi.size());
+    upload(P.xs_cbase, cbase.data(), cbase.size());
+    P.xs_clusters = static_cast<int>(clo.size());
+    P.xs_tab_len = static_cast<int>(tl);
+    P.xs_bytes = static_cast<int>((bytes + 15) / 16 * 16);
+    return true;
 }
 
 template <class T, int L, bool PAT>
 void* sell_fn_LP(int u) {
     switch (u) {
         case 4: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 4>);
+        case 9: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 9>);
         case 12: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 12>);
+        case 14: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 14>);
         default: return reinterpret_cast<void*>(&dev::k_gather_sell<T, L, PAT, 8>);
     }
 }
@@ -712,7 +779,7 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const std:
     const double avg = n ? static_cast<double>(eptr[n]) / n : 0.0;
     // lanes per row: rows of <= 40 entries (27-point stencils) split over 2
     // lanes, longer rows (81-entry elasticity) one lane (profiles/r01_sweep_sell*.txt)
-    const int L = env_int("CSRC_GPU_SELL_L", avg <= 40 ? 2 : 1);
+    const int L = env_int("CSRC_GPU_SELL_L", 1);  // 2 / 4 lanes lost on every config (r01_sweep_sell2.txt)
     P.sell_lanes = (L == 2 || L == 4) ? L : 1;
     const int H = 32 / P.sell_lanes;
     const int64_t ns = (static_cast<int64_t>(n) + H - 1) / H;
@@ -756,7 +823,7 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const std:
     else upload(P.sidx, sidx.data(), sidx.size());
     if (!pat) P.n_patterns = 0;
     const int u = env_int("CSRC_GPU_SELL_U", 8);
-    P.sell_u = (u == 4 || u == 12) ? u : 8;
+    P.sell_u = (u == 4 || u == 9 || u == 12 || u == 14) ? u : 8;
     P.gather_sell = 1;
     P.gather_buf = 0;
     P.sell_pat_len = pat ? static_cast<int>(pat_off.size()) : 0;
@@ -866,10 +933,12 @@ void setup_gather(Plan& P, const MatView& a) {
     P.gather_nt = env_int("CSRC_GPU_GNT", 256) == 128 ? 128 : 256;
     P.gather_minb = env_int("CSRC_GPU_GMINB", 1) == 8 ? 8 : 1;
     std::vector<int32_t> pbase, pat_off;
-    if (env_int("CSRC_GPU_GPATTERN", 1) != 0 && P.gather_lanes <= 8)
-        P.gather_pat = find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns) ? 1 : 0;
+    const bool has_pat = P.gather_lanes <= 8 && find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns);
+    P.gather_pat = has_pat && env_int("CSRC_GPU_GPATTERN", 1) != 0 ? 1 : 0;
     if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 2 && P.gather_lanes <= 8) {
         const int R = P.gather_nt / P.gather_lanes;
+        // staged x (pattern form): x windows of each row block come in by TMA with the values
+        P.gather_xs = P.gather_pat && env_int("CSRC_GPU_GXS", 1) != 0 && setup_staged_x<T>(P, pat_off) ? 1 : 0;
         int64_t cap = 0;
         for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
         if (cap <= 16384) {
@@ -893,7 +962,13 @@ void setup_gather(Plan& P, const MatView& a) {
             }
         }
     }
-    if (env_int("CSRC_GPU_GSELL", 1) != 0 && n > 0) {
+    // sliced form for rows longer than ~40 entries with a small pattern dictionary
+    // (C4 elasticity: 281 us vs 365 us staged); the staged form stays ahead on
+    // 27-point rows (C5: 694 vs 705 us f64, 466 vs 565 us f32) and on explicit
+    // columns (C3) -- profiles/r01_sweep_sell3.txt. CSRC_GPU_GSELL=0/1 forces.
+    const int sell_env = env_int("CSRC_GPU_GSELL", -1);
+    const bool sell_auto = has_pat && avg > 40.0;  // (not P.gather_pat: explicit columns keep the same form)
+    if ((sell_env == 1 || (sell_env < 0 && sell_auto)) && n > 0) {
         setup_sell<T>(P, n, eptr, eidx, ev, evt, a.value_symmetric, pbase, pat_off);
         return;
     }
@@ -972,6 +1047,22 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
         A.nrows = r1;
         A.idx_bytes = P.gather_pat ? 0 : dev::gather_idx_bytes(P.gather_cap);
         A.val_bytes = dev::gather_val_bytes<T>(P.gather_cap);
+        A.xs_tab = nullptr;
+        A.clo = A.chi = A.cbase = nullptr;
+        A.n_clusters = 0;
+        A.x_min = P.lo - P.row_begin;  // x holds [lo, x_hi) global = these kernel coordinates
+        A.x_max = P.x_hi - P.row_begin;
+        A.xs_bytes = 0;
+        if (P.gather_xs) {
+            const int m = 16 / static_cast<int>(sizeof(T));
+            const int ph = static_cast<int>((reinterpret_cast<uintptr_t>(x) / sizeof(T)) % m);
+            A.xs_tab = P.xs_tab.as<int32_t>() + static_cast<size_t>(ph) * P.xs_tab_len;
+            A.clo = P.xs_clo.as<int32_t>();
+            A.chi = P.xs_chi.as<int32_t>();
+            A.cbase = P.xs_cbase.as<int32_t>();
+            A.n_clusters = P.xs_clusters;
+            A.xs_bytes = P.xs_bytes;
+        }
         const int64_t blocks = (static_cast<int64_t>(r1 - r0) + R - 1) / R;
         const int grid = static_cast<int>(std::min<int64_t>(blocks, P.gather_grid));
         void* args[] = {&A};
@@ -1589,7 +1680,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t, &P.xs_tab, &P.xs_clo, &P.xs_chi, &P.xs_cbase})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS
@@ -1626,6 +1717,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
                                                                          : gather_stage_smem<float>(P))
                                             : 0;
         }
+        info->gather_form = P.exec_kind != CSRC_KIND_GATHER ? 0 : P.gather_sell ? 3 : P.gather_buf ? 2 : 1;
         info->m_cols = P.m_cols;
         info->rect_nnz = P.rect_nnz;
         if (P.m_cols) {

@@ -124,6 +124,19 @@ struct GStageArgs {
     int32_t nrows;
     int32_t idx_bytes;  // per buffer, 16-aligned (0 when PAT)
     int32_t val_bytes;  // per buffer, 16-aligned
+    // XS (pattern form with staged x): the plan groups the stencil's column
+    // offsets into K clusters [clo_k, chi_k]; a row block [q0, q0 + R) then
+    // reads x only on the K windows [q0 + clo_k, q0 + R + chi_k), which thread 0
+    // copies next to the values (cluster k at element cbase_k of the x area);
+    // xs_tab[pattern entry] = cbase_k + alignment pad + (offset - clo_k), so the
+    // x value of entry f of local row rl is x_area[xs_tab[.] + rl] (LDS).
+    const int32_t* xs_tab;
+    const int32_t* clo;
+    const int32_t* chi;
+    const int32_t* cbase;
+    int32_t n_clusters;
+    int32_t x_min, x_max;  // readable x range (kernel coordinates)
+    int32_t xs_bytes;      // x area per buffer, 16-aligned
 };
 
 // shared-memory bytes of one buffer holding up to `cap` entries (+ alignment slack)
@@ -133,14 +146,16 @@ __host__ __device__ inline int gather_val_bytes(int cap) {
     return ((cap + 8) * static_cast<int>(sizeof(T)) + 15) & ~15;
 }
 
-template <typename T, int L, int U, int NB, bool PAT, int MINB>
+template <typename T, int L, int U, int NB, int PF, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T> A) {
     static_assert(NB == 1 || NB == 2, "one or two row-block buffers");
+    constexpr bool PAT = PF >= 1;  // PF: 0 explicit columns, 1 row patterns, 2 patterns + staged x
+    constexpr bool XS = PF == 2;
     extern __shared__ __align__(128) unsigned char smem[];
     const int R = blockDim.x / L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2]
     unsigned char* bufs = smem + 16;
-    const int buf_bytes = A.idx_bytes + A.val_bytes;
+    const int buf_bytes = A.idx_bytes + A.val_bytes + (XS ? A.xs_bytes : 0);
     const int sub = threadIdx.x % L;
     const int rrel = threadIdx.x / L;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * R;
@@ -153,9 +168,32 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
             e1 = __ldg(A.eptr + (b + R < A.nrows ? b + R : A.nrows));
         }
     };
-    auto issue = [&](int buf, int32_t e0, int32_t e1) {
+    auto issue = [&](int buf, int32_t e0, int32_t e1, int64_t q0) {
         unsigned char* st = bufs + buf * buf_bytes;
         const Seg<T> sv = seg(A.eval, e0, e1);
+        if (XS) {
+            // value span + the K x windows of row block [q0, q0 + R), clamped to
+            // the readable x range (the clamped-off slots are never read)
+            unsigned char* xa = st + A.idx_bytes + A.val_bytes;
+            uint32_t bytes = sv.bytes;
+            for (int k = 0; k < A.n_clusters; ++k) {
+                const int64_t s0 = q0 + __ldg(A.clo + k), s1 = q0 + R + __ldg(A.chi + k);
+                const int64_t c0 = s0 > A.x_min ? s0 : A.x_min, c1 = s1 < A.x_max ? s1 : A.x_max;
+                if (c0 < c1) bytes += seg(A.x, c0, c1).bytes;
+            }
+            mbar_expect_tx(&full[buf], bytes);
+            tma_load(st + A.idx_bytes, sv.src, sv.bytes, &full[buf]);
+            for (int k = 0; k < A.n_clusters; ++k) {
+                const int64_t s0 = q0 + __ldg(A.clo + k), s1 = q0 + R + __ldg(A.chi + k);
+                const int64_t c0 = s0 > A.x_min ? s0 : A.x_min, c1 = s1 < A.x_max ? s1 : A.x_max;
+                if (c0 >= c1) continue;
+                const Seg<T> sx = seg(A.x, c0, c1);
+                const uintptr_t ua = reinterpret_cast<uintptr_t>(A.x + s0) & ~uintptr_t(15);
+                tma_load(xa + sizeof(T) * __ldg(A.cbase + k) + (reinterpret_cast<uintptr_t>(sx.src) - ua), sx.src,
+                         sx.bytes, &full[buf]);
+            }
+            return;
+        }
         if (PAT) {
             mbar_expect_tx(&full[buf], sv.bytes);
         } else {
@@ -172,7 +210,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         if (first < A.nrows) {
             int32_t e0 = 0, e1 = 0;
             span(first, e0, e1);
-            issue(0, e0, e1);
+            issue(0, e0, e1, first);
         }
         span(first + stride, nx0, nx1);
     }
@@ -183,7 +221,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     for (int64_t base = first; base < A.nrows; base += stride, ++it) {
         const int buf = NB == 2 ? (it & 1) : 0;
         if (NB == 2 && threadIdx.x == 0 && base + stride < A.nrows) {
-            issue(buf ^ 1, nx0, nx1);  // buffer buf^1 was released by the last __syncthreads
+            issue(buf ^ 1, nx0, nx1, base + stride);  // buffer buf^1 was released by the last __syncthreads
             span(base + 2 * stride, nx0, nx1);
         }
         const int64_t row = base + rrel;
@@ -204,6 +242,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         const uint32_t vb = st + A.idx_bytes -
                             static_cast<uint32_t>(sizeof(T)) * static_cast<uint32_t>(e_base & ~(kValAlign - 1));
         const T* xrow = A.x + row;
+        const uint32_t xb = st + A.idx_bytes + A.val_bytes + static_cast<uint32_t>(sizeof(T)) * rrel;
         T acc0 = T(0), acc1 = T(0);
         for (int32_t e = eb + sub; e < ee; e += U * L) {
             T xv[U];
@@ -211,7 +250,10 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
             for (int u = 0; u < U; ++u) {
                 const int32_t f = e + u * L;
                 xv[u] = T(0);
-                if (f < ee) xv[u] = PAT ? __ldg(xrow + __ldg(A.pat_off + pb + f)) : __ldg(A.x + lds_i(ib + 4u * f));
+                if (f < ee)
+                    xv[u] = XS    ? lds_f(xb + static_cast<uint32_t>(sizeof(T)) * __ldg(A.xs_tab + pb + f), T())
+                            : PAT ? __ldg(xrow + __ldg(A.pat_off + pb + f))
+                                  : __ldg(A.x + lds_i(ib + 4u * f));
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -230,7 +272,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         if (act && sub == 0) A.y[row] = s + d * xr;
         __syncthreads();
         if (NB == 1 && threadIdx.x == 0 && base + stride < A.nrows) {
-            issue(0, nx0, nx1);  // single buffer: refill once every thread is done with it
+            issue(0, nx0, nx1, base + stride);  // single buffer: refill once every thread is done with it
             span(base + 2 * stride, nx0, nx1);
         }
     }
@@ -305,7 +347,7 @@ struct GSellArgs {
 };
 
 // resident 256-thread blocks per SM the register budget is sized for
-template <int U> struct SellMinBlocks { static constexpr int value = U <= 4 ? 4 : U <= 8 ? 3 : 2; };
+template <int U> struct SellMinBlocks { static constexpr int value = U <= 4 ? 4 : U <= 9 ? 3 : 2; };
 
 template <typename T, int L, bool PAT, int U>
 __global__ void __launch_bounds__(256, SellMinBlocks<U>::value) k_gather_sell(const GSellArgs<T> A) {

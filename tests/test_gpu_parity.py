@@ -351,6 +351,14 @@ GATHER_SHAPES = [
     {"CSRC_GPU_GNB": "2", "CSRC_GPU_GLANES": "2", "CSRC_GPU_GU": "8"},
     {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "8", "CSRC_GPU_GU": "4"},
     {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "16", "CSRC_GPU_GU": "8"},
+    # sliced (SELL) form: lanes per row, steps in flight, pattern / explicit columns
+    {"CSRC_GPU_GSELL": "1"},
+    {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_L": "2"},
+    {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_L": "4", "CSRC_GPU_SELL_U": "4"},
+    {"CSRC_GPU_GSELL": "1", "CSRC_GPU_GPATTERN": "0", "CSRC_GPU_SELL_U": "12"},
+    {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_U": "9"},
+    {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_U": "14", "CSRC_GPU_SELL_L": "2"},
+    {"CSRC_GPU_GSELL": "0"},
 ]
 
 
@@ -374,6 +382,43 @@ def test_gather_kernel_shapes(shape, monkeypatch):
         p = f"m{idx}_"
         a = FAM.matrix(p)
         assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.gather)), FAM[p + "y"]) <= TOL64
+
+
+@pytest.mark.parametrize("lanes", ["1", "2"])
+def test_sliced_form_bands_pipeline_and_bits(lanes, monkeypatch):
+    """The sliced gather form (k_gather_sell) on band plans, through the host
+    pipeline (row chunks = whole slices) and with explicit columns: the same
+    bits as the pattern form, oracle parity for y and y^T."""
+    import torch
+    monkeypatch.setenv("CSRC_GPU_GSELL", "1")
+    monkeypatch.setenv("CSRC_GPU_SELL_L", lanes)
+    a = MESH.matrix("g2_")
+    x = MESH["g2_x"]
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    assert ex.info().gather_form == 3
+    y = ex.apply(x)
+    yt = ex.apply(x, transpose=True)
+    ex.close()
+    assert rel_l2(y, MESH["g2_y"]) <= TOL64
+    assert rel_l2(yt, O.spmv_csrc(a, x, transpose=True)) <= TOL64
+    monkeypatch.setenv("CSRC_GPU_GPATTERN", "0")
+    ex = P.GpuSpmv(a, P.Strategy(K.gather))
+    assert ex.info().row_patterns == 0 and ex.info().gather_form == 3
+    assert np.array_equal(ex.apply(x), y)
+    ex.close()
+    part = P.partition_by_nnz(a, 3)
+    yb = np.zeros(a.n)
+    xd = torch.from_numpy(x).cuda()
+    for b in range(3):
+        r0, r1 = part.begin(b), part.end(b)
+        eb = P.GpuSpmv(a, P.Strategy(K.gather), band=(r0, r1))
+        inf = eb.info()
+        yd = torch.empty(r1 - r0, dtype=torch.float64, device="cuda")
+        eb.apply_device(xd[inf.lo:inf.x_hi].contiguous(), yd)
+        torch.cuda.synchronize()
+        yb[r0:r1] = yd.cpu().numpy()
+        eb.close()
+    assert rel_l2(yb, MESH["g2_y"]) <= TOL64
 
 
 def test_gather_dense_row_falls_back():
