@@ -14,7 +14,8 @@ reference (file:line)                      here
 =========================================  ======================================
 
 All of these run on ``device`` (default 0) and fail with :class:`Error` when
-no GPU is present; there is no host fallback.
+no GPU is present; there is no host fallback. Results are zero-copy numpy
+views of the library's host arrays; the handle is freed with the last view.
 """
 from __future__ import annotations
 
@@ -41,10 +42,26 @@ def _ptr(a: np.ndarray, t):
     return a.ctypes.data_as(C.POINTER(t)) if a.size else None
 
 
-def _copy(p, count: int, dt) -> np.ndarray:
+class _Owner:
+    """Keeps a csrc_built_t alive while numpy views of its host arrays exist."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def __del__(self):
+        try:
+            L.built_free(self.h)
+        except Exception:
+            pass
+
+
+def _view(p, count: int, ctype, dt, owner: _Owner) -> np.ndarray:
+    """Zero-copy numpy view of `count` elements at `p`, owned by the handle."""
     if count == 0:
         return np.zeros(0, dt)
-    return np.ctypeslib.as_array(p, shape=(count,)).astype(dt, copy=True)
+    buf = (ctype * count).from_address(C.cast(p, C.c_void_p).value)
+    buf._owner = owner  # the array's base keeps the handle alive
+    return np.frombuffer(buf, dtype=dt)
 
 
 @dataclass
@@ -111,15 +128,16 @@ def _triplet_args(t, n_rows=None, n_cols=None):
             np.ascontiguousarray(c, np.int32), np.ascontiguousarray(v, np.float64))
 
 
-def _csrc_from_handle(h):
+def _csrc_from_handle(h, owner: _Owner):
     from . import CsrcMatrix
     m = L.HostMatrix()
     _check(L.built_matrix(h, C.byref(m)))
     n, k = m.n, m.k
     sym = bool(m.value_symmetric)
-    return CsrcMatrix(n, _copy(m.ad, n, np.float64), _copy(m.ia, n + 1, np.int32),
-                      _copy(m.ja, k, np.int32), _copy(m.al, k, np.float64),
-                      np.zeros(0) if sym else _copy(m.au, k, np.float64), sym)
+    f, i = C.c_double, C.c_int32
+    return CsrcMatrix(n, _view(m.ad, n, f, np.float64, owner), _view(m.ia, n + 1, i, np.int32, owner),
+                      _view(m.ja, k, i, np.int32, owner), _view(m.al, k, f, np.float64, owner),
+                      np.zeros(0) if sym else _view(m.au, k, f, np.float64, owner), sym)
 
 
 def _timings(h) -> dict:
@@ -136,15 +154,14 @@ def build_csr(t, device: int = 0) -> CsrMatrix:
     h = C.c_void_p()
     _check(L.build_csr(nr, nc, r.size, _ptr(r, C.c_int32), _ptr(c, C.c_int32), _ptr(v, C.c_double),
                        device, C.byref(h)))
-    try:
-        n_rows, n_cols, nnz = C.c_int32(), C.c_int32(), C.c_int64()
-        rp, ci, va = L.P_i32(), L.P_i32(), L.P_f64()
-        _check(L.built_csr(h, C.byref(n_rows), C.byref(n_cols), C.byref(nnz), C.byref(rp), C.byref(ci),
-                           C.byref(va)))
-        return CsrMatrix(n_rows.value, n_cols.value, _copy(rp, n_rows.value + 1, np.int32),
-                         _copy(ci, nnz.value, np.int32), _copy(va, nnz.value, np.float64))
-    finally:
-        L.built_free(h)
+    owner = _Owner(h)
+    n_rows, n_cols, nnz = C.c_int32(), C.c_int32(), C.c_int64()
+    rp, ci, va = L.P_i32(), L.P_i32(), L.P_f64()
+    _check(L.built_csr(h, C.byref(n_rows), C.byref(n_cols), C.byref(nnz), C.byref(rp), C.byref(ci),
+                       C.byref(va)))
+    return CsrMatrix(n_rows.value, n_cols.value, _view(rp, n_rows.value + 1, C.c_int32, np.int32, owner),
+                     _view(ci, nnz.value, C.c_int32, np.int32, owner),
+                     _view(va, nnz.value, C.c_double, np.float64, owner))
 
 
 def build_csrc(t, device: int = 0, timings: dict = None):
@@ -155,12 +172,10 @@ def build_csrc(t, device: int = 0, timings: dict = None):
     h = C.c_void_p()
     _check(L.build_csrc(nr, r.size, _ptr(r, C.c_int32), _ptr(c, C.c_int32), _ptr(v, C.c_double), device,
                         C.byref(h)))
-    try:
-        if timings is not None:
-            timings.update(_timings(h))
-        return _csrc_from_handle(h)
-    finally:
-        L.built_free(h)
+    owner = _Owner(h)
+    if timings is not None:
+        timings.update(_timings(h))
+    return _csrc_from_handle(h, owner)
 
 
 def csr_to_csrc(a: CsrMatrix, device: int = 0):
@@ -171,10 +186,7 @@ def csr_to_csrc(a: CsrMatrix, device: int = 0):
     h = C.c_void_p()
     _check(L.csr_to_csrc(int(a.n_rows), int(a.n_cols), rp.ctypes.data_as(L.P_i32), _ptr(ci, C.c_int32),
                          _ptr(va, C.c_double), device, C.byref(h)))
-    try:
-        return _csrc_from_handle(h)
-    finally:
-        L.built_free(h)
+    return _csrc_from_handle(h, _Owner(h))
 
 
 def decompose_rect(a: CsrMatrix, device: int = 0) -> CsrcRectMatrix:
@@ -185,16 +197,15 @@ def decompose_rect(a: CsrMatrix, device: int = 0) -> CsrcRectMatrix:
     h = C.c_void_p()
     _check(L.decompose_rect(int(a.n_rows), int(a.n_cols), rp.ctypes.data_as(L.P_i32), _ptr(ci, C.c_int32),
                             _ptr(va, C.c_double), device, C.byref(h)))
-    try:
-        sq = _csrc_from_handle(h)
-        m, nnz = C.c_int32(), C.c_int64()
-        trp, tci, tva = L.P_i32(), L.P_i32(), L.P_f64()
-        _check(L.built_rect_tail(h, C.byref(m), C.byref(nnz), C.byref(trp), C.byref(tci), C.byref(tva)))
-        tail = CsrMatrix(sq.n, m.value - sq.n, _copy(trp, sq.n + 1, np.int32), _copy(tci, nnz.value, np.int32),
-                         _copy(tva, nnz.value, np.float64))
-        return CsrcRectMatrix(sq, tail, m.value)
-    finally:
-        L.built_free(h)
+    owner = _Owner(h)
+    sq = _csrc_from_handle(h, owner)
+    m, nnz = C.c_int32(), C.c_int64()
+    trp, tci, tva = L.P_i32(), L.P_i32(), L.P_f64()
+    _check(L.built_rect_tail(h, C.byref(m), C.byref(nnz), C.byref(trp), C.byref(tci), C.byref(tva)))
+    tail = CsrMatrix(sq.n, m.value - sq.n, _view(trp, sq.n + 1, C.c_int32, np.int32, owner),
+                     _view(tci, nnz.value, C.c_int32, np.int32, owner),
+                     _view(tva, nnz.value, C.c_double, np.float64, owner))
+    return CsrcRectMatrix(sq, tail, m.value)
 
 
 def csrc_to_triplets(a) -> Tuple[int, int, np.ndarray, np.ndarray, np.ndarray]:

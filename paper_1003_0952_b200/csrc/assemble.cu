@@ -41,27 +41,53 @@
 #include <memory>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.hpp"
 
 using namespace csrcgpu;
 
+namespace {
+// Host vectors without value-initialisation: resize() leaves the pages
+// untouched, so the multithreaded copy-out below takes the first-touch page
+// faults in parallel instead of a serial zero fill.
+template <class T>
+struct NoInit : std::allocator<T> {
+    using value_type = T;
+    template <class U>
+    struct rebind { using other = NoInit<U>; };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) {}
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        if constexpr (sizeof...(A) == 0) {
+            ::new (static_cast<void*>(p)) U;
+        } else {
+            ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+        }
+    }
+};
+template <class T>
+using HVec = std::vector<T, NoInit<T>>;
+}  // namespace
+
 struct csrc_built_s {
     // CSR (build_csr) and/or CSRC (csr_to_csrc); host arrays owned here
     int has_csr = 0, has_csrc = 0;
     index_t n_rows = 0, n_cols = 0;
-    std::vector<index_t> row_ptr, col_idx;
-    std::vector<double> values;
+    HVec<index_t> row_ptr, col_idx;
+    HVec<double> values;
     index_t n = 0;
-    std::vector<double> ad, al, au;
-    std::vector<index_t> ia, ja;
+    HVec<double> ad, al, au;
+    HVec<index_t> ia, ja;
     int value_symmetric = 0;
     // rectangular tail (decompose_rect): CSR over columns n..m-1, local indices
     int has_rect = 0;
     index_t m_cols = 0;
-    std::vector<index_t> t_row_ptr, t_col_idx;
-    std::vector<double> t_values;
+    HVec<index_t> t_row_ptr, t_col_idx;
+    HVec<double> t_values;
     double ms[4] = {0, 0, 0, 0};  // h2d, sort+reduce, convert, d2h
 };
 
@@ -254,16 +280,106 @@ __global__ void k_csrc(int64_t nnz, const index_t* __restrict__ rp, const index_
 }
 
 // ------------------------------------------------------------- helpers
+// Pageable host <-> device copies at link speed: two pinned staging buffers;
+// the DMA of one chunk overlaps the multithreaded host memcpy of the next.
+// (cudaMemcpy from pageable memory ran at 11 GB/s up and 2.7 GB/s down into
+// fresh vectors at C5, profiles/r01_assemble_gpu.jsonl.)
+void pmemcpy(void* dst, const void* src, size_t bytes) {
+    const size_t kMinPerThread = size_t(4) << 20;
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int t = static_cast<int>(std::min<size_t>(std::min(hw, 16), std::max<size_t>(1, bytes / kMinPerThread)));
+    if (t <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    std::vector<std::thread> pool;
+    const size_t part = (bytes / t + 63) & ~size_t(63);
+    for (int i = 0; i < t; ++i) {
+        const size_t o = static_cast<size_t>(i) * part;
+        if (o >= bytes) break;
+        const size_t len = std::min(part, bytes - o);
+        pool.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, len); });
+    }
+    for (auto& th : pool) th.join();
+}
+
+class HostLink {
+public:
+    static constexpr size_t kStage = size_t(64) << 20;
+    explicit HostLink(cudaStream_t st) : st_(st) {}
+    ~HostLink() {
+        for (int b = 0; b < 2; ++b) {
+            if (buf_[b]) cudaFreeHost(buf_[b]);
+            if (ev_[b]) cudaEventDestroy(ev_[b]);
+        }
+    }
+    HostLink(const HostLink&) = delete;
+    HostLink& operator=(const HostLink&) = delete;
+
+    void h2d(void* dev, const void* host, size_t bytes) {
+        if (bytes <= kSmall) {
+            if (bytes) ACUDA(cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
+            return;
+        }
+        ready();
+        size_t c = 0;
+        for (size_t off = 0; off < bytes; off += kStage, ++c) {
+            const size_t len = std::min(kStage, bytes - off);
+            const int b = static_cast<int>(c & 1);
+            if (c >= 2) ACUDA(cudaEventSynchronize(ev_[b]));  // the DMA that last read buffer b
+            pmemcpy(buf_[b], static_cast<const char*>(host) + off, len);
+            ACUDA(cudaMemcpyAsync(static_cast<char*>(dev) + off, buf_[b], len, cudaMemcpyHostToDevice, st_));
+            ACUDA(cudaEventRecord(ev_[b], st_));
+        }
+        ACUDA(cudaStreamSynchronize(st_));
+    }
+
+    void d2h(void* host, const void* dev, size_t bytes) {
+        if (bytes <= kSmall) {
+            if (bytes) ACUDA(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost));
+            return;
+        }
+        ready();
+        const size_t nc = (bytes + kStage - 1) / kStage;
+        auto issue = [&](size_t c) {
+            const size_t off = c * kStage, len = std::min(kStage, bytes - off);
+            const int b = static_cast<int>(c & 1);
+            ACUDA(cudaMemcpyAsync(buf_[b], static_cast<const char*>(dev) + off, len, cudaMemcpyDeviceToHost, st_));
+            ACUDA(cudaEventRecord(ev_[b], st_));
+        };
+        issue(0);
+        for (size_t c = 0; c < nc; ++c) {
+            if (c + 1 < nc) issue(c + 1);  // its buffer was drained by the host copy of chunk c - 1
+            const int b = static_cast<int>(c & 1);
+            ACUDA(cudaEventSynchronize(ev_[b]));
+            const size_t off = c * kStage;
+            pmemcpy(static_cast<char*>(host) + off, buf_[b], std::min(kStage, bytes - off));
+        }
+    }
+
+private:
+    static constexpr size_t kSmall = size_t(8) << 20;
+    void ready() {
+        for (int b = 0; b < 2; ++b) {
+            if (!buf_[b]) ACUDA(cudaHostAlloc(&buf_[b], kStage, cudaHostAllocDefault));
+            if (!ev_[b]) ACUDA(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t st_;
+    void* buf_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
+
 template <class T>
-void h2d(DMem& d, const T* h, int64_t count) {
+void h2d(HostLink& hl, DMem& d, const T* h, int64_t count) {
     d.alloc(static_cast<size_t>(count) * sizeof(T));
-    if (count) ACUDA(cudaMemcpy(d.p, h, static_cast<size_t>(count) * sizeof(T), cudaMemcpyHostToDevice));
+    if (count) hl.h2d(d.p, h, static_cast<size_t>(count) * sizeof(T));
 }
 
 template <class T>
-void d2h(std::vector<T>& h, const DMem& d, int64_t count) {
+void d2h(HostLink& hl, HVec<T>& h, const DMem& d, int64_t count) {
     h.resize(static_cast<size_t>(count));
-    if (count) ACUDA(cudaMemcpy(h.data(), d.p, static_cast<size_t>(count) * sizeof(T), cudaMemcpyDeviceToHost));
+    if (count) hl.d2h(h.data(), d.p, static_cast<size_t>(count) * sizeof(T));
 }
 
 unsigned long long read_u64(const DMem& d) {
@@ -360,7 +476,7 @@ void check_bounds(index_t n_rows, index_t n_cols, int64_t m, const DMem& r, cons
 }
 
 // csr_to_csrc (csrc_matrix.hpp:44-91) on a device CSR with erow.
-void csr_to_csrc_dev(const DevCsr& a, csrc_built_s& out, cudaStream_t st, double* ms_conv,
+void csr_to_csrc_dev(const DevCsr& a, csrc_built_s& out, cudaStream_t st, HostLink& hl, double* ms_conv,
                      double* ms_d2h) {
     Clock clk;
     if (a.n_rows != a.n_cols) throw Error("csr_to_csrc: matrix is not square");
@@ -410,20 +526,19 @@ void csr_to_csrc_dev(const DevCsr& a, csrc_built_s& out, cudaStream_t st, double
     out.has_csrc = 1;
     out.n = n;
     out.value_symmetric = asym_h ? 0 : 1;
-    d2h(out.ad, ad, n);
-    d2h(out.ia, ia, static_cast<int64_t>(n) + 1);
-    d2h(out.ja, ja, k);
-    d2h(out.al, al, k);
-    if (!out.value_symmetric) d2h(out.au, au, k);
+    d2h(hl, out.ad, ad, n);
+    d2h(hl, out.ia, ia, static_cast<int64_t>(n) + 1);
+    d2h(hl, out.ja, ja, k);
+    d2h(hl, out.al, al, k);
+    if (!out.value_symmetric) d2h(hl, out.au, au, k);
     else out.au.clear();
     *ms_d2h += clk.lap();
 }
 
-void csr_to_host(const DevCsr& a, std::vector<index_t>& rp, std::vector<index_t>& col,
-                 std::vector<double>& val) {
-    d2h(rp, a.rp, static_cast<int64_t>(a.n_rows) + 1);
-    d2h(col, a.col, a.nnz);
-    d2h(val, a.val, a.nnz);
+void csr_to_host(HostLink& hl, const DevCsr& a, HVec<index_t>& rp, HVec<index_t>& col, HVec<double>& val) {
+    d2h(hl, rp, a.rp, static_cast<int64_t>(a.n_rows) + 1);
+    d2h(hl, col, a.col, a.nnz);
+    d2h(hl, val, a.val, a.nnz);
 }
 
 struct DeviceScope {
@@ -466,11 +581,12 @@ int csrc_gpu_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t*
         DeviceScope ds(device);
         Stream st;
         auto b = std::make_unique<csrc_built_s>();
+        HostLink hl(st.s);
         Clock clk;
         DMem r, c, v;
-        h2d(r, rows, m);
-        h2d(c, cols, m);
-        h2d(v, vals, m);
+        h2d(hl, r, rows, m);
+        h2d(hl, c, cols, m);
+        h2d(hl, v, vals, m);
         b->ms[0] = clk.lap();
         check_bounds(n_rows, n_cols, m, r, c, rows, cols, st.s);
         DevCsr csr;
@@ -479,7 +595,7 @@ int csrc_gpu_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t*
         b->has_csr = 1;
         b->n_rows = n_rows;
         b->n_cols = n_cols;
-        csr_to_host(csr, b->row_ptr, b->col_idx, b->values);
+        csr_to_host(hl, csr, b->row_ptr, b->col_idx, b->values);
         b->ms[3] = clk.lap();
         *out = b.release();
     });
@@ -495,11 +611,12 @@ int csrc_gpu_build_csrc(int32_t n, int64_t m, const int32_t* rows, const int32_t
         DeviceScope ds(device);
         Stream st;
         auto b = std::make_unique<csrc_built_s>();
+        HostLink hl(st.s);
         Clock clk;
         DMem r, c, v;
-        h2d(r, rows, m);
-        h2d(c, cols, m);
-        h2d(v, vals, m);
+        h2d(hl, r, rows, m);
+        h2d(hl, c, cols, m);
+        h2d(hl, v, vals, m);
         b->ms[0] = clk.lap();
         check_bounds(n, n, m, r, c, rows, cols, st.s);
         DevCsr csr;
@@ -507,7 +624,7 @@ int csrc_gpu_build_csrc(int32_t n, int64_t m, const int32_t* rows, const int32_t
         r.release();
         c.release();
         v.release();
-        csr_to_csrc_dev(csr, *b, st.s, &b->ms[2], &b->ms[3]);
+        csr_to_csrc_dev(csr, *b, st.s, hl, &b->ms[2], &b->ms[3]);
         *out = b.release();
     });
 }
@@ -525,21 +642,22 @@ int csrc_gpu_csr_to_csrc(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
         DeviceScope ds(device);
         Stream st;
         auto b = std::make_unique<csrc_built_s>();
+        HostLink hl(st.s);
         Clock clk;
         DevCsr csr;
         csr.n_rows = n_rows;
         csr.n_cols = n_cols;
         csr.nnz = nnz;
-        h2d(csr.rp, row_ptr, static_cast<int64_t>(n_rows) + 1);
-        h2d(csr.col, col_idx, nnz);
-        h2d(csr.val, values, nnz);
+        h2d(hl, csr.rp, row_ptr, static_cast<int64_t>(n_rows) + 1);
+        h2d(hl, csr.col, col_idx, nnz);
+        h2d(hl, csr.val, values, nnz);
         csr.erow.alloc(static_cast<size_t>(nnz) * 4);
         b->ms[0] = clk.lap();
         if (n_rows > 0) {
             k_erow<<<grid_for(n_rows), 256, 0, st.s>>>(n_rows, csr.rp.as<index_t>(), csr.erow.as<index_t>());
             ACUDA(cudaGetLastError());
         }
-        csr_to_csrc_dev(csr, *b, st.s, &b->ms[2], &b->ms[3]);
+        csr_to_csrc_dev(csr, *b, st.s, hl, &b->ms[2], &b->ms[3]);
         *out = b.release();
     });
 }

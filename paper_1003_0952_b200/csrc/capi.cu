@@ -938,7 +938,7 @@ void setup_gather(Plan& P, const MatView& a) {
     if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 2 && P.gather_lanes <= 8) {
         const int R = P.gather_nt / P.gather_lanes;
         // staged x (pattern form): x windows of each row block come in by TMA with the values
-        P.gather_xs = P.gather_pat && env_int("CSRC_GPU_GXS", 1) != 0 && setup_staged_x<T>(P, pat_off) ? 1 : 0;
+        P.gather_xs = P.gather_pat && env_int("CSRC_GPU_GXS", 0) != 0 && setup_staged_x<T>(P, pat_off) ? 1 : 0;
         int64_t cap = 0;
         for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
         if (cap <= 16384) {
