@@ -20,8 +20,9 @@ for name in cfgs:
     print(f'== {name} n={a.n} k={a.k_off()} gen {tg:.2f}s oracle {to:.2f}s model {mb/1e6:.1f} MB', flush=True)
     xd = torch.from_numpy(x).cuda(); yd = torch.zeros_like(xd)
     for kn, kind, acc in kinds:
-        if kind == P.StrategyKind.colorful and a.n > 5_000_000: continue
-        if kind == P.StrategyKind.local_buffers and a.n > 5_000_000 and acc in (0, 1): continue
+        big = a.n > 5_000_000 and not os.environ.get('ALLBIG')
+        if kind == P.StrategyKind.colorful and big: continue
+        if kind == P.StrategyKind.local_buffers and big and acc in (0, 1): continue
         try:
             t = time.time(); ex = P.GpuSpmv(a, P.Strategy(kind, P.AccumMethod(acc), p=8)); tp = time.time() - t
             y = ex.apply(x)
