@@ -138,6 +138,7 @@ struct csrc_gpu_plan_s {
     std::vector<int32_t> hchunk;
     std::vector<int32_t> hneed;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaStream_t s_h2d2 = nullptr, s_d2h2 = nullptr;  // optional second copy streams
     cudaEvent_t ev_in = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
 
@@ -187,6 +188,8 @@ struct csrc_gpu_plan_s {
         if (ev_in) cudaEventDestroy(ev_in);
         if (s_h2d) cudaStreamDestroy(s_h2d);
         if (s_d2h) cudaStreamDestroy(s_d2h);
+        if (s_h2d2) cudaStreamDestroy(s_h2d2);
+        if (s_d2h2) cudaStreamDestroy(s_d2h2);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -898,7 +901,17 @@ void setup_gather(Plan& P, const MatView& a) {
         P.hchunk.clear();
         const int forced = env_int("CSRC_GPU_HOST_CHUNKS", 0);
         std::vector<int> units;
-        if (forced > 0)
+        if (const char* us = std::getenv("CSRC_GPU_HOST_UNITS")) {  // e.g. "1,2,4,8,8,4,2,1"
+            for (const char* q = us; *q;) {
+                const int u = std::atoi(q);
+                if (u > 0) units.push_back(u);
+                while (*q && *q != ',') ++q;
+                if (*q == ',') ++q;
+            }
+        }
+        if (!units.empty())
+            ;
+        else if (forced > 0)
             units.assign(forced, 1);
         else if (n >= (int64_t(1) << 20))
             units = {2, 4, 8, 8, 8, 8, 8, 8, 4, 2, 2, 1, 1};
@@ -1459,6 +1472,8 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
     if (!P.s_h2d) {
         CUDA_OK(cudaStreamCreateWithFlags(&P.s_h2d, cudaStreamNonBlocking));
         CUDA_OK(cudaStreamCreateWithFlags(&P.s_d2h, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&P.s_h2d2, cudaStreamNonBlocking));
+        CUDA_OK(cudaStreamCreateWithFlags(&P.s_d2h2, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreateWithFlags(&P.ev_in, cudaEventDisableTiming));
         P.ev_x.assign(nc, nullptr);
         P.ev_y.assign(nc, nullptr);
@@ -1484,13 +1499,19 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         for (auto& e : tr_ev) CUDA_OK(cudaEventCreate(&e));
         CUDA_OK(cudaEventRecord(tr_ev[0], st));
     }
+    // CSRC_GPU_HOST_H2D_STREAMS / _D2H_STREAMS = 2: alternate chunks over two
+    // copy streams per direction (diagnostics; default one each)
+    const bool h2d2 = env_int("CSRC_GPU_HOST_H2D_STREAMS", 1) == 2;
+    const bool d2h2 = env_int("CSRC_GPU_HOST_D2H_STREAMS", 1) == 2;
     CUDA_OK(cudaEventRecord(P.ev_in, st));
     CUDA_OK(cudaStreamWaitEvent(P.s_h2d, P.ev_in, 0));  // after earlier work on the plan stream
+    if (h2d2) CUDA_OK(cudaStreamWaitEvent(P.s_h2d2, P.ev_in, 0));
     for (int c = 0; c < nc; ++c) {
         const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
-        CUDA_OK(cudaMemcpyAsync(xd64 + r0, xh + r0, len * 8, cudaMemcpyHostToDevice, P.s_h2d));
-        CUDA_OK(cudaEventRecord(P.ev_x[c], P.s_h2d));
-        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + c], P.s_h2d));
+        cudaStream_t sc = h2d2 && (c & 1) ? P.s_h2d2 : P.s_h2d;
+        CUDA_OK(cudaMemcpyAsync(xd64 + r0, xh + r0, len * 8, cudaMemcpyHostToDevice, sc));
+        CUDA_OK(cudaEventRecord(P.ev_x[c], sc));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + c], sc));
     }
     int have = -1;  // x chunks the compute stream already waited for (and converted)
     for (int c = 0; c < nc; ++c) {
@@ -1513,12 +1534,15 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaEventRecord(P.ev_y[c], st));
         if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + nc + c], st));
-        CUDA_OK(cudaStreamWaitEvent(P.s_d2h, P.ev_y[c], 0));
+        cudaStream_t sd = d2h2 && (c & 1) ? P.s_d2h2 : P.s_d2h;
+        CUDA_OK(cudaStreamWaitEvent(sd, P.ev_y[c], 0));
         CUDA_OK(cudaMemcpyAsync(yh + r0, yd64 + r0, static_cast<size_t>(r1 - r0) * 8,
-                                cudaMemcpyDeviceToHost, P.s_d2h));
-        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + 2 * nc + c], P.s_d2h));
+                                cudaMemcpyDeviceToHost, sd));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + 2 * nc + c], sd));
     }
     CUDA_OK(cudaStreamSynchronize(P.s_d2h));
+    if (d2h2) CUDA_OK(cudaStreamSynchronize(P.s_d2h2));
+    if (h2d2) CUDA_OK(cudaStreamSynchronize(P.s_h2d2));
     CUDA_OK(cudaStreamSynchronize(st));
     if (trace) {
         std::fprintf(stderr, "host pipeline: %d chunks (ms from start: x landed / rows done / y landed)\n", nc);
