@@ -229,6 +229,17 @@ int csrc_gpu_band_split(csrc_gpu_plan_t plan, int32_t* boundary_rows_end);
 int csrc_gpu_spmv_device_part(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream,
                               int32_t part);
 
+/* Gather plans: rows [*rows_begin, *rows_end) (relative to the plan's rows,
+ * 256-aligned inward) read x only on the plan's own rows -- for band plans
+ * they can run while an x-halo exchange is in flight (paper_1003_0952_b200.dist). */
+int csrc_gpu_gather_interior(csrc_gpu_plan_t plan, int32_t* rows_begin, int32_t* rows_end);
+
+/* Gather plans: the product restricted to rows [rows_begin, rows_end) (plan-relative;
+ * begin a multiple of 256, end a multiple of 256 or the last row); d_x / d_y as for
+ * csrc_gpu_spmv_device, only the range's y rows are written. flags bit 0: transpose. */
+int csrc_gpu_spmv_device_rows(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream, int32_t flags,
+                              int32_t rows_begin, int32_t rows_end);
+
 /* csrc::ParallelSpmv::last_timings (parallel.hpp:222); synchronises on the
  * last apply's events. Timing events are recorded only when enabled. */
 int csrc_gpu_set_timing(csrc_gpu_plan_t plan, int32_t enabled);

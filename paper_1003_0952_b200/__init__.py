@@ -497,6 +497,19 @@ class GpuSpmv:
         _check(L.halo_accumulate(self._h, self._ptr(y), dst_off, self._ptr(recv), length,
                                  st or None))
 
+    def gather_interior(self) -> Tuple[int, int]:
+        """Rows (plan-relative) that read x only on the plan's own rows."""
+        a, b = C.c_int32(), C.c_int32()
+        _check(L.gather_interior(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def apply_device_rows(self, x, y, rows_begin: int, rows_end: int, stream=None,
+                          transpose: bool = False) -> None:
+        """Gather plans: the product on rows [rows_begin, rows_end) only."""
+        st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
+        _check(L.spmv_device_rows(self._h, self._ptr(x), self._ptr(y), st or None, 1 if transpose else 0,
+                                  int(rows_begin), int(rows_end)))
+
     def band_split(self) -> int:
         v = C.c_int32()
         _check(L.band_split(self._h, C.byref(v)))

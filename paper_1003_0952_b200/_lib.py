@@ -131,6 +131,8 @@ spmv_device_graph = _sig("csrc_gpu_spmv_device_graph", C.c_int, vp, vp, vp, vp)
 spmv_device_part = _sig("csrc_gpu_spmv_device_part", C.c_int, vp, vp, vp, vp, i32)
 halo_accumulate = _sig("csrc_gpu_halo_accumulate", C.c_int, vp, vp, i64, vp, i64, vp)
 band_split = _sig("csrc_gpu_band_split", C.c_int, vp, P_i32)
+gather_interior = _sig("csrc_gpu_gather_interior", C.c_int, vp, P_i32, P_i32)
+spmv_device_rows = _sig("csrc_gpu_spmv_device_rows", C.c_int, vp, vp, vp, vp, i32, i32, i32)
 set_timing = _sig("csrc_gpu_set_timing", C.c_int, vp, i32)
 last_timings = _sig("csrc_gpu_last_timings", C.c_int, vp, C.POINTER(Timings))
 time_products = _sig("csrc_gpu_time_products", C.c_int, vp, vp, vp, i32, i64, P_f64, P_f64)
@@ -177,6 +179,7 @@ EXPORTED = [
     "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
+    "csrc_gpu_gather_interior", "csrc_gpu_spmv_device_rows",
     "csrc_gpu_spmv_device_part", "csrc_gpu_set_timing", "csrc_gpu_last_timings",
     "csrc_gpu_time_products", "csrc_gpu_time_products_host", "csrc_partition_by_nnz", "csrc_effective_ranges",
     "csrc_interval_plan", "csrc_color_rows", "csrc_conflict_edge_counts",

@@ -176,6 +176,9 @@ struct csrc_gpu_plan_s {
     index_t x_len() const { return m_cols ? m_cols : n_global; }
     index_t vec_len() const { return row_end - lo; }
     index_t x_hi = 0;  // gather: end of the x range the plan reads (band plans: above row_end)
+    // gather band plans: rows [gi0, gi1) (band-relative, 256-aligned inward) read
+    // x only on the band's own rows -- they can run before an x-halo exchange lands
+    index_t gi0 = 0, gi1 = 0;
     int launches = 0;
 
     ~csrc_gpu_plan_s() {
@@ -885,6 +888,18 @@ void setup_gather(Plan& P, const MatView& a) {
             ev[w] = a.value_symmetric ? a.al[t] : a.au[t];
             if (!a.value_symmetric) evt[w] = a.al[t];
         }
+    {
+        // interior rows of a band: all columns inside the band's own rows [0, n)
+        index_t b0 = 0, b1 = n;
+        for (index_t q = 0; q < n; ++q)
+            for (int32_t e = eptr[q]; e < eptr[q + 1]; ++e) {
+                if (eidx[e] < 0) b0 = std::max(b0, q + 1);
+                if (eidx[e] >= n) b1 = std::min(b1, q);
+            }
+        const index_t a0 = (b0 + 255) / 256 * 256, a1 = b1 == n ? n : b1 / 256 * 256;
+        P.gi0 = std::min(a0, n);
+        P.gi1 = std::max(P.gi0, a1);
+    }
     upload(P.eptr, eptr.data(), eptr.size());
     upload_values<T>(P.eval, ev.data(), ev.size());
     if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
@@ -1825,6 +1840,40 @@ int csrc_gpu_halo_accumulate(csrc_gpu_plan_t plan, void* d_y, int64_t dst_off,
         else
             dev::k_halo_add<float><<<grid_for(P.device, len, 256), 256, 0, st>>>(
                 static_cast<float*>(d_y) + dst_off, static_cast<const float*>(d_recv), len);
+        CUDA_OK(cudaGetLastError());
+    });
+}
+
+int csrc_gpu_gather_interior(csrc_gpu_plan_t plan, int32_t* rows_begin, int32_t* rows_end) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (P.exec_kind != CSRC_KIND_GATHER) throw Error("interior rows are defined for gather plans");
+        *rows_begin = P.gi0;
+        *rows_end = P.gi1;
+    });
+}
+
+int csrc_gpu_spmv_device_rows(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream, int32_t flags,
+                              int32_t rows_begin, int32_t rows_end) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (P.exec_kind != CSRC_KIND_GATHER) throw Error("row-range products need a gather plan");
+        if (P.m_cols) throw Error("row-range products need a square plan");
+        if (rows_begin < 0 || rows_end > P.nrows || rows_begin > rows_end)
+            throw Error("row range [" + std::to_string(rows_begin) + ", " + std::to_string(rows_end) +
+                        ") outside the plan's " + std::to_string(P.nrows) + " rows");
+        if (rows_begin == rows_end || P.nrows == 0) return;
+        if (rows_begin % 256 != 0 || (rows_end % 256 != 0 && rows_end != P.nrows))
+            throw Error("row ranges start on a multiple of 256 and end on one or at the last row");
+        CUDA_OK(cudaSetDevice(P.device));
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
+        const bool tr = (flags & 1) != 0 && !P.value_symmetric;
+        if (P.dtype == CSRC_DTYPE_F64)
+            launch_gather_range<double>(P, tr, static_cast<const double*>(d_x), static_cast<double*>(d_y),
+                                        rows_begin, rows_end, st);
+        else
+            launch_gather_range<float>(P, tr, static_cast<const float*>(d_x), static_cast<float*>(d_y), rows_begin,
+                                       rows_end, st);
         CUDA_OK(cudaGetLastError());
     });
 }

@@ -7,6 +7,12 @@ Two band forms:
   pairs) and above it (the rows that name it as a column), so x is replicated
   over [lo_g, x_hi_g) and the rank writes exactly its own y rows: no y
   exchange at all (weak-scaling shards, no data-path collective).
+  For repeated products (an iterative solver feeding y back as x) each rank
+  owns only x on its rows; ``apply_device(..., refresh_x=True)`` then
+  exchanges the x halo [lo_g, row_begin) ∪ [row_end, x_hi_g) with grouped
+  NCCL send/recv on a communication stream while the band's interior rows
+  (``csrc_gpu_gather_interior``: rows reading only own x) run, and finishes
+  the boundary rows once the halo has landed (``csrc_gpu_spmv_device_rows``).
 * windowed (scatter): the y-halo reduce below.
 
 Rank g owns rows [block_start[g], block_start[g+1]) of
@@ -60,6 +66,10 @@ class HaloPlan:
     x_hi: int = -1
     y_lo: int = -1
     mode: str = "windowed"
+    # gather form, x-halo refresh: (peer, q0, q1) global x positions I send
+    # (my rows in peer's x range) / receive (peer's rows in my x range)
+    x_sends: List[Tuple[int, int, int]] = dataclasses.field(default_factory=list)
+    x_recvs: List[Tuple[int, int, int]] = dataclasses.field(default_factory=list)
 
     def __post_init__(self):
         if self.x_hi < 0:
@@ -89,13 +99,41 @@ def band_x_hi(a: CsrcMatrix, r0: int, r1: int) -> int:
     return int(max(r1, rows[m].max() + 1)) if m.any() else int(r1)
 
 
-def gather_plan(a: CsrcMatrix, world: int, rank: int, x_hi: Optional[int] = None) -> HaloPlan:
-    """Gather-form band of rank `rank`: no exchange, x over [lo, x_hi)."""
+def bands_x_hi(a: CsrcMatrix, block_start: List[int]) -> List[int]:
+    """band_x_hi for every band of a partition (one pass over the pairs)."""
+    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.ia))
+    out = []
+    for b in range(len(block_start) - 1):
+        r0, r1 = block_start[b], block_start[b + 1]
+        m = (a.ja >= r0) & (a.ja < r1)
+        out.append(int(max(r1, rows[m].max() + 1)) if m.any() else int(r1))
+    return out
+
+
+def gather_plan(a: CsrcMatrix, world: int, rank: int, x_hi: Optional[int] = None,
+                all_x_hi: Optional[List[int]] = None) -> HaloPlan:
+    """Gather-form band of rank `rank`: x over [lo, x_hi), own y rows only.
+    The x-halo lists say which x rows move between ranks when only the owned
+    rows of x are current (refresh_x)."""
     part = partition_by_nnz(a, world)
     ranges = effective_ranges(a, part)
-    r0, r1 = part.begin(rank), part.end(rank)
-    hi = band_x_hi(a, r0, r1) if x_hi is None else x_hi
-    return HaloPlan(rank, world, r0, r1, ranges[rank].lo, [], [], x_hi=hi, y_lo=r0, mode="gather")
+    bs = [part.begin(b) for b in range(world)] + [a.n]
+    his = all_x_hi if all_x_hi is not None else bands_x_hi(a, bs)
+    r0, r1 = bs[rank], bs[rank + 1]
+    hi = his[rank] if x_hi is None else x_hi
+    lo = ranges[rank].lo
+    x_sends, x_recvs = [], []
+    for b in range(world):
+        if b == rank:
+            continue
+        q0, q1 = max(lo, bs[b]), min(hi, bs[b + 1])  # peer b's rows inside my x range
+        if q0 < q1:
+            x_recvs.append((b, q0, q1))
+        q0, q1 = max(ranges[b].lo, r0), min(his[b], r1)  # my rows inside peer b's x range
+        if q0 < q1:
+            x_sends.append((b, q0, q1))
+    return HaloPlan(rank, world, r0, r1, lo, [], [], x_hi=hi, y_lo=r0, mode="gather",
+                    x_sends=x_sends, x_recvs=x_recvs)
 
 
 def halo_plan(a: CsrcMatrix, world: int, rank: int) -> HaloPlan:
@@ -148,6 +186,7 @@ class DistSpmv:
                 self.ex = GpuSpmv(a, s, band=(r0, r1))
                 x_hi = int(self.ex.info().x_hi)
             self.plan = gather_plan(a, self.world, self.rank, x_hi)
+            assert self.plan.x_hi == (x_hi if x_hi is not None else self.plan.x_hi)
         else:
             self.plan = halo_plan(a, self.world, self.rank)
             if band_compute is None:
@@ -163,6 +202,25 @@ class DistSpmv:
             self.ex = None
 
     # -------------------------------------------------------------- exchange
+    def _post_x(self, x_local):
+        """Grouped P2P of the x halo (gather form): my rows to the peers whose
+        x range covers them, the peers' rows into my halo slices."""
+        dist = self.dist
+        p = self.plan
+        ops = []
+        for peer, q0, q1 in p.x_sends:
+            ops.append(dist.P2POp(dist.isend, x_local[q0 - p.x_lo:q1 - p.x_lo], peer, self.group))
+        for peer, q0, q1 in p.x_recvs:
+            ops.append(dist.P2POp(dist.irecv, x_local[q0 - p.x_lo:q1 - p.x_lo], peer, self.group))
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def exchange_x(self, x_local):
+        """Blocking x-halo refresh: afterwards x_local holds current x on
+        [x_lo, x_hi) given current values on the owned rows."""
+        for w in self._post_x(x_local):
+            w.wait()
+        return x_local
+
     def _post(self, y_local, recv_bufs):
         dist = self.dist
         p = self.plan
@@ -173,11 +231,13 @@ class DistSpmv:
             ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
         return dist.batch_isend_irecv(ops) if ops else []
 
-    def apply_host(self, x_local, y_local):
+    def apply_host(self, x_local, y_local, refresh_x: bool = False):
         """Host mode (gloo): band product via the injected callable."""
         import torch
 
         p = self.plan
+        if refresh_x and self.mode == "gather":
+            self.exchange_x(x_local)
         y_local.copy_(torch.as_tensor(self.band_compute(p, x_local.numpy())))
         if self.mode == "gather":
             return y_local  # own rows only, nothing to exchange
@@ -188,12 +248,36 @@ class DistSpmv:
             y_local[q0 - p.lo:q1 - p.lo] += buf
         return y_local
 
-    def apply_device(self, x_local, y_local, overlap: bool = True):
+    def apply_device(self, x_local, y_local, overlap: bool = True, refresh_x: bool = False):
         import torch
 
         p = self.plan
         if self.mode == "gather":
-            self.ex.apply_device(x_local, y_local)
+            if not refresh_x or (not p.x_sends and not p.x_recvs):
+                self.ex.apply_device(x_local, y_local)
+                return y_local
+            if self._streams is None:
+                self._streams = (torch.cuda.current_stream(), torch.cuda.Stream())
+                self._ev_halo = torch.cuda.Event()
+                self._ev_recv = torch.cuda.Event()
+                self._interior = self.ex.gather_interior()
+            comp, comm = self._streams
+            g0, g1 = self._interior
+            n_rows = p.row_end - p.row_begin
+            self._ev_halo.record(comp)  # owned x rows are current on the compute stream
+            comm.wait_event(self._ev_halo)
+            with torch.cuda.stream(comm):
+                for w in self._post_x(x_local):
+                    w.wait()
+                self._ev_recv.record(comm)
+            if overlap and g0 < g1:
+                self.ex.apply_device_rows(x_local, y_local, g0, g1, comp)  # interior: own x only
+                comp.wait_event(self._ev_recv)
+                self.ex.apply_device_rows(x_local, y_local, 0, g0, comp)
+                self.ex.apply_device_rows(x_local, y_local, g1, n_rows, comp)
+            else:
+                comp.wait_event(self._ev_recv)
+                self.ex.apply_device(x_local, y_local, comp)
             return y_local
         if self._streams is None:
             self._streams = (torch.cuda.current_stream(), torch.cuda.Stream())

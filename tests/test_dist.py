@@ -49,7 +49,7 @@ def _gather_band_product(a, plan, x_local):
     return Oracle().spmv_csrc(a, x)[plan.row_begin:plan.row_end]
 
 
-def _worker(rank, world, port, mesh_key, out_q, mode="windowed"):
+def _worker(rank, world, port, mesh_key, out_q, mode="windowed", refresh=False):
     import torch
     import torch.distributed as dist
     from paper_1003_0952_b200.dist import DistSpmv
@@ -67,21 +67,30 @@ def _worker(rank, world, port, mesh_key, out_q, mode="windowed"):
         p = ds.plan
         assert p.mode == mode
         xl = torch.from_numpy(x[p.x_lo:p.x_hi].copy())
+        if refresh:  # only the owned x rows are current; the halo comes from the peers
+            xl[:] = float("nan")
+            xl[p.row_begin - p.x_lo:p.row_end - p.x_lo] = torch.from_numpy(x[p.row_begin:p.row_end])
         yl = torch.zeros(p.row_end - p.y_lo, dtype=torch.float64)
-        ds.apply_host(xl, yl)
+        ds.apply_host(xl, yl, refresh_x=refresh)
+        if refresh:
+            assert np.array_equal(xl.numpy(), x[p.x_lo:p.x_hi])
         out_q.put((rank, p.row_begin, p.row_end, yl.numpy()[p.row_begin - p.y_lo:].copy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["windowed", "gather"])
+@pytest.mark.parametrize("mode", ["windowed", "gather", "gather_refresh"])
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("mesh_key", ["g1_", "g3_", "g5_"])
 def test_gloo_band_exchange_reassembles_the_product(world, mesh_key, mode):
+    """gather_refresh: each rank starts with x current only on its own rows and
+    the x halo arrives through the grouped P2P exchange (iterative use)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_key, q, mode)) for r in range(world)]
+    refresh = mode == "gather_refresh"
+    mode = "gather" if refresh else mode
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_key, q, mode, refresh)) for r in range(world)]
     for pr in procs:
         pr.start()
     parts = [q.get(timeout=120) for _ in range(world)]
@@ -125,3 +134,23 @@ def test_gather_plan_ranges():
             upper_rows = rows[(a.ja >= p.row_begin) & (a.ja < p.row_end)]
             assert upper_rows.size == 0 or upper_rows.max() < p.x_hi
             assert p.x_hi == band_x_hi(a, p.row_begin, p.row_end) >= p.row_end
+
+
+def test_gather_x_halo_lists_are_consistent():
+    """Every x row a rank receives is sent by its owner, exactly once, and the
+    received pieces tile the rank's x range minus its own rows."""
+    m = meshes()
+    a = m.matrix("g5_")
+    for world in (2, 3, 5, 8):
+        plans = [gather_plan(a, world, r) for r in range(world)]
+        sends = sorted((r, peer, q0, q1) for r, p in enumerate(plans) for peer, q0, q1 in p.x_sends)
+        recvs = sorted((peer, r, q0, q1) for r, p in enumerate(plans) for peer, q0, q1 in p.x_recvs)
+        assert sends == recvs
+        for p in plans:
+            covered = np.zeros(a.n, np.int32)
+            covered[p.row_begin:p.row_end] += 1
+            for peer, q0, q1 in p.x_recvs:
+                assert plans[peer].row_begin <= q0 < q1 <= plans[peer].row_end
+                covered[q0:q1] += 1
+            assert np.all(covered[p.x_lo:p.x_hi] == 1)
+            assert covered[:p.x_lo].sum() == 0 and covered[p.x_hi:].sum() == 0

@@ -319,6 +319,50 @@ def test_band_plans_assemble_the_product(bands, mesh):
     assert rel_l2(y, MESH[mesh + "y"]) <= TOL64
 
 
+@pytest.mark.parametrize("cfg", ["c2", "c4"])
+@pytest.mark.parametrize("bands", [2, 3])
+def test_gather_interior_rows_overlap_form(cfg, bands):
+    """x-halo refresh form of the gather bands (dist.DistSpmv refresh_x): the
+    interior rows run while the x halo is still garbage (NaN), the boundary
+    rows after it lands; the result equals the one-shot band product bit for
+    bit and the oracle."""
+    import torch
+    a, x, _ = P.config_matrix(cfg)
+    ref = O.spmv_csrc(a, x)
+    part = P.partition_by_nnz(a, bands)
+    xd = torch.from_numpy(x).cuda()
+    for b in range(bands):
+        r0, r1 = part.begin(b), part.end(b)
+        ex = P.GpuSpmv(a, P.Strategy(K.gather), band=(r0, r1))
+        inf = ex.info()
+        g0, g1 = ex.gather_interior()
+        assert 0 <= g0 <= g1 <= r1 - r0 and g0 % 256 == 0
+        assert g1 > g0, "bands of these meshes have interior rows"
+        full = torch.empty(r1 - r0, dtype=torch.float64, device="cuda")
+        xl = xd[inf.lo:inf.x_hi].contiguous()
+        ex.apply_device(xl, full)
+        halo = xl.clone()
+        halo[: r0 - inf.lo] = float("nan")
+        halo[r1 - inf.lo:] = float("nan")
+        y = torch.full((r1 - r0,), float("nan"), dtype=torch.float64, device="cuda")
+        ex.apply_device_rows(halo, y, g0, g1)
+        torch.cuda.synchronize()
+        assert not torch.isnan(y[g0:g1]).any()
+        halo.copy_(xl)
+        ex.apply_device_rows(halo, y, 0, g0)
+        ex.apply_device_rows(halo, y, g1, r1 - r0)
+        torch.cuda.synchronize()
+        assert torch.equal(y, full)
+        assert rel_l2(y.cpu().numpy(), ref[r0:r1]) <= TOL64
+        with pytest.raises(P.Error, match="multiple of 256"):
+            ex.apply_device_rows(halo, y, 1, g1)
+        ex.close()
+    ex = P.GpuSpmv(a, P.Strategy(K.windowed))
+    with pytest.raises(P.Error, match="gather plan"):
+        ex.apply_device_rows(xd, xd, 0, 256)
+    ex.close()
+
+
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
 def test_host_pipeline_matches_device(cfg):
     """The host entry point of a gather plan overlaps the x upload, the row
