@@ -93,6 +93,7 @@ struct csrc_gpu_plan_s {
     int n_tiles = 0;
     int near_depth = 0, far_lo = 1, far_hi = 0, ring_near = 1, ring_far = 0;
     int max_tile_pairs = 16;
+    bool win_ring = false; // shared-memory rings (CSRC_GPU_WIN_RINGS=1), else red.global only
     size_t win_smem = 0;
     int win_lanes = 1;     // L lanes per row in the windowed kernel
     int tile_rows = 128;   // rows per tile (64 or 128)
@@ -213,6 +214,18 @@ void upload_values(DevBuf& d, const double* h, size_t count) {
     }
 }
 
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);  // tuning knobs for sweeps
+    return e ? std::atoi(e) : dflt;
+}
+
+// Shared-memory rings for the windowed kernel's scatters (CSRC_GPU_WIN_RINGS=1).
+// Off by default: sm_100a has no native shared-memory FP add, every ring update
+// is an ATOMS.CAS loop, and the L2's native red.global.add.f64 is faster --
+// C5 1.09 ms without rings vs 1.60 ms with, C4 0.65 vs 2.12, C3 0.27 vs 0.94
+// (profiles/r01_sweep_windowed_rings.txt, r01_sweep_windowed_no_rings.txt).
+bool win_rings() { return env_int("CSRC_GPU_WIN_RINGS", 0) != 0; }
+
 // --------------------------------------------------- windowed schedule
 // Ring windows from the histogram of scatter distances d = row - ja: the
 // near ring covers 1..Dn (plus the own row), the far ring the densest
@@ -262,6 +275,12 @@ void choose_windows(Plan& P, const MatView& a) {
         }
     }
     P.captured = total ? static_cast<double>(near_cnt + far_cnt) / total : 1.0;
+    if (!win_rings()) {  // default: every scatter to red.global (win_rings)
+        P.near_depth = 0;
+        P.far_lo = 1;
+        P.far_hi = 0;
+        P.captured = 0.0;
+    }
 }
 
 // Tiles (<= kTileRows rows, <= max_tile_pairs pairs) over bands given as
@@ -342,6 +361,11 @@ dev::StageLayout<T> stage_layout(const Plan& P) {
 // rings hold the window plus every tile that can be live: the one awaiting
 // its lagged flush and up to `stages` in flight (windowed.cuh)
 void size_rings(Plan& P, int stages) {
+    if (!P.win_ring) {  // ring-free kernel: no shared-memory windows at all
+        P.ring_near = 0;
+        P.ring_far = 0;
+        return;
+    }
     const int live = (stages + 1) * P.tile_rows;
     P.ring_near = pow2_at_least(P.near_depth + live);
     P.ring_far = P.far_lo <= P.far_hi ? pow2_at_least(P.far_hi - P.far_lo + 1 + live) : 0;
@@ -354,32 +378,37 @@ size_t windowed_smem(const Plan& P, int stages) {
     return (s + 127) & ~size_t(127);
 }
 
-template <class T>
-auto windowed_fn(int L, int TR) {
+template <class T, bool R>
+auto windowed_fn_R(int L, int TR) {
     if (TR == 32) {
         switch (L) {
-            case 1: return dev::k_windowed<T, 1, 32>;
-            case 2: return dev::k_windowed<T, 2, 32>;
-            default: return dev::k_windowed<T, 4, 32>;
+            case 1: return dev::k_windowed<T, 1, 32, R>;
+            case 2: return dev::k_windowed<T, 2, 32, R>;
+            default: return dev::k_windowed<T, 4, 32, R>;
         }
     }
     if (TR == 64) {
         switch (L) {
-            case 1: return dev::k_windowed<T, 1, 64>;
-            case 2: return dev::k_windowed<T, 2, 64>;
-            default: return dev::k_windowed<T, 4, 64>;
+            case 1: return dev::k_windowed<T, 1, 64, R>;
+            case 2: return dev::k_windowed<T, 2, 64, R>;
+            default: return dev::k_windowed<T, 4, 64, R>;
         }
     }
     switch (L) {
-        case 1: return dev::k_windowed<T, 1, 128>;
-        case 2: return dev::k_windowed<T, 2, 128>;
-        default: return dev::k_windowed<T, 4, 128>;
+        case 1: return dev::k_windowed<T, 1, 128, R>;
+        case 2: return dev::k_windowed<T, 2, 128, R>;
+        default: return dev::k_windowed<T, 4, 128, R>;
     }
 }
 
 template <class T>
+auto windowed_fn(int L, int TR, bool rings) {
+    return rings ? windowed_fn_R<T, true>(L, TR) : windowed_fn_R<T, false>(L, TR);
+}
+
+template <class T>
 int windowed_blocks_per_sm(const Plan& P, size_t smem) {
-    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows);
+    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows, P.win_ring);
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
     int nb = 0;
@@ -397,23 +426,29 @@ MatView local_view(const MatView& a, index_t r0, index_t r1) {
     return v;
 }
 
-int pick_win_lanes(count_t k, index_t n) {  // see profiles/r01_sweep10.txt
-    // measured on B200 (profiles/r01_sweep*.txt): ~6 pairs per lane is best
+int pick_win_lanes(count_t k, index_t n, bool rings) {
     const double avg = n ? static_cast<double>(k) / n : 0.0;
+    if (!rings) {
+        // scatters straight to red.global: more lanes per row = more reds in
+        // flight; 4 lanes won on C3 / C4 / C5 (profiles/r01_sweep_windowed_no_rings.txt)
+        if (avg <= 3) return 1;
+        if (avg <= 6) return 2;
+        return 4;
+    }
+    // smem rings (profiles/r01_sweep10.txt): ~6 pairs per lane is best
     if (avg <= 6) return 1;
     if (avg <= 16) return 2;
     return 4;  // CTA = producer warp + 128*L consumer threads <= 1024
 }
 
-int env_int(const char* name, int dflt) {
-    const char* e = std::getenv(name);  // tuning knobs for sweeps
-    return e ? std::atoi(e) : dflt;
-}
+
+
 
 template <class T>
 void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
                     int requested_bands, bool banded) {
-    P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows));
+    P.win_ring = win_rings();
+    P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows, P.win_ring));
     if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4)
         throw Error("windowed lanes per row must be 1, 2 or 4");
     {   // ~1.7K pairs (~35 KB of fp64 matrix data) per tile: big TMA copies
@@ -1352,7 +1387,7 @@ template <class T>
 void launch_windowed(const Plan& P, dev::WinArgs<T> A, int ctas, cudaStream_t st) {
     if (ctas <= 0) return;
     if (P.value_symmetric) A.au = A.al;
-    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows);
+    auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows, P.win_ring);
     // per-plan shared-memory size: the attribute is per function, so set it per launch
     CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(P.win_smem)));

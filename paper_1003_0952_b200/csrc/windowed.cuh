@@ -243,7 +243,10 @@ __device__ __forceinline__ void flush_tile(const WinArgs<T>& A, T* __restrict__ 
     if (far_on) flush(ringF, A.ring_far - 1, g0 - A.far_hi, end ? g1 - A.far_lo : g1 - A.far_hi);
 }
 
-template <typename T, int L, int TR>
+// RINGS = false (the default, capi.cu win_rings): no shared-memory windows --
+// every scatter and every row result is a red.global.add; no ring zeroing, no
+// done barriers, no flush.
+template <typename T, int L, int TR, bool RINGS>
 __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const StageLayout<T> lay(A.max_tile_pairs, 0, 0, TR);
@@ -272,7 +275,8 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
     const int bank_elems = A.ring_near + A.ring_far;
     T* rings = reinterpret_cast<T*>(smem_raw + S * A.stage_bytes);
 
-    for (int i = tid; i < 2 * bank_elems; i += blockDim.x) rings[i] = T(0);
+    if (RINGS)
+        for (int i = tid; i < 2 * bank_elems; i += blockDim.x) rings[i] = T(0);
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
@@ -337,7 +341,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
         const int s = ti % S;
         // lagged flush: tile ti-1 is flushed by consumer warp (ti-1) % W once
         // every consumer warp has finished it
-        if (ti >= 1 && (ti - 1) % kConsumerWarps == cw) {
+        if (RINGS && ti >= 1 && (ti - 1) % kConsumerWarps == cw) {
             mbar_wait(&done[(ti - 1) % kDoneSlots], ((ti - 1) / kDoneSlots) & 1);
             flush_tile(A, out, rings, bank_elems, dring[(ti - 1) % kDoneSlots], lane);
             __syncwarp();
@@ -396,6 +400,10 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
                     if (j[u] >= 0) {
                         yi = fma(lds_f(al_b + E * mm[u], T(0)), xv[u], yi);
                         val[u] = lds_f(au_b + E * mm[u], T(0)) * xi;
+                        if (!RINGS) {
+                            red_add(out + j[u], val[u]);
+                            continue;
+                        }
                         const int32_t d = g - j[u];
                         if (d <= near_depth)
                             sa[u] = ringN_s + E * static_cast<uint32_t>(j[u] & maskN);
@@ -405,6 +413,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
                             red_add(out + j[u], val[u]);
                     }
                 }
+                if (!RINGS) continue;
                 if (L == 1) {
                     T old[4];  // four independent CAS in flight
 #pragma unroll
@@ -438,7 +447,8 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
         // all lanes reach the width-L reduction (rows >= nr contribute 0)
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) yi += __shfl_xor_sync(0xffffffffu, yi, off, L);
-        if (act && sub == 0) {
+        if (!RINGS && act && sub == 0) red_add(out + g, yi + lds_f(ad_b + E * row, T(0)) * xi);
+        if (RINGS && act && sub == 0) {
             const uint32_t a = ringN_s + static_cast<uint32_t>(g & maskN) * sizeof(T);
             const T add = yi + lds_f(ad_b + E * row, T(0)) * xi;
             T old0 = lds_f(a, T(0));
@@ -454,12 +464,12 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
         __syncwarp();
         if (lane == 0) {
             mbar_arrive(&empty[s]);                   // stage s may be refilled
-            mbar_arrive(&done[ti % kDoneSlots]);      // tile ti's ring contributions are in
+            if (RINGS) mbar_arrive(&done[ti % kDoneSlots]);  // tile ti's ring contributions are in
         }
     }
     // the last tile's flush
     const int tl = t_count - 1;
-    if (tl % kConsumerWarps == cw) {
+    if (RINGS && tl % kConsumerWarps == cw) {
         mbar_wait(&done[tl % kDoneSlots], (tl / kDoneSlots) & 1);
         flush_tile(A, out, rings, bank_elems, dring[tl % kDoneSlots], lane);
     }

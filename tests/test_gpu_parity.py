@@ -428,6 +428,31 @@ def test_gather_kernel_shapes(shape, monkeypatch):
         assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.gather)), FAM[p + "y"]) <= TOL64
 
 
+@pytest.mark.parametrize("lanes", ["1", "2", "4"])
+def test_windowed_shared_memory_rings(lanes, monkeypatch):
+    """The windowed kernel's optional shared-memory rings (CSRC_GPU_WIN_RINGS=1:
+    in-window scatters resolved by CAS adds in shared memory, flushed with
+    red.global; off by default because red.global alone is faster on B200)
+    still give the product, also under the local-buffers accumulations and on
+    band plans."""
+    monkeypatch.setenv("CSRC_GPU_WIN_RINGS", "1")
+    monkeypatch.setenv("CSRC_GPU_LANES", lanes)
+    for idx in (1, 2, 3, 5):
+        p = f"g{idx}_"
+        a = MESH.matrix(p)
+        ex = P.GpuSpmv(a, P.Strategy(K.windowed))
+        assert ex.info().captured_fraction > 0
+        assert rel_l2(ex.apply(MESH[p + "x"]), MESH[p + "y"]) <= TOL64
+        ex.close()
+        for acc in (A.effective, A.interval):
+            y = run(a, MESH[p + "x"], P.Strategy(K.local_buffers, acc, p=4))
+            assert rel_l2(y, MESH[p + "y"]) <= TOL64
+    for idx in range(0, 29, 7):
+        p = f"m{idx}_"
+        a = FAM.matrix(p)
+        assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.windowed)), FAM[p + "y"]) <= TOL64
+
+
 @pytest.mark.parametrize("lanes", ["1", "2"])
 def test_sliced_form_bands_pipeline_and_bits(lanes, monkeypatch):
     """The sliced gather form (k_gather_sell) on band plans, through the host
