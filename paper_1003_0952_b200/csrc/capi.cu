@@ -429,11 +429,10 @@ MatView local_view(const MatView& a, index_t r0, index_t r1) {
 int pick_win_lanes(count_t k, index_t n, bool rings) {
     const double avg = n ? static_cast<double>(k) / n : 0.0;
     if (!rings) {
-        // scatters straight to red.global: more lanes per row = more reds in
-        // flight; 4 lanes won on C3 / C4 / C5 (profiles/r01_sweep_windowed_no_rings.txt)
-        if (avg <= 3) return 1;
-        if (avg <= 6) return 2;
-        return 4;
+        // ring-free kernel (scatters straight to red.global): 2 lanes per row
+        // won on C2-C5 (C5 0.852 ms vs 0.871 at 4 lanes, C4 0.598 vs 0.656;
+        // profiles/r01_sweep_windowed_ringfree.txt)
+        return avg <= 3 ? 1 : 2;
     }
     // smem rings (profiles/r01_sweep10.txt): ~6 pairs per lane is best
     if (avg <= 6) return 1;

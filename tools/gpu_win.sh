@@ -1,7 +1,5 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_dropin_cpp.py tests/test_gpu_rect.py -m gpu -q -x -k "windowed or lb_ or local or band or rings or dropin or rect or known or meshes" > gpurun_out/pytest_win.log 2>&1; echo "pytest rc=$?"; tail -5 gpurun_out/pytest_win.log
-for v in 'CSRC_GPU_LANES=4' 'CSRC_GPU_LANES=4 CSRC_GPU_STAGES=2' 'CSRC_GPU_LANES=2' 'CSRC_GPU_LANES=4 CSRC_GPU_MINCTAS=3'; do
-  echo "## $v"
-  for cfg in c5 c4 c3 c2; do env $v KINDS=windowed,lb_interval NOF32=1 timeout 300 python tools/gpu_probe.py $cfg 2>&1 | grep -E "^  [a-z]" | sed "s/^/$cfg /"; done
-done | tee gpurun_out/sweep_win3.txt
+timeout 600 python bench.py --kind windowed --no-cpu-baseline --compare atomic,local_buffers > gpurun_out/bench_win.json 2> gpurun_out/bench.err; echo "bench win rc=$?"; cat gpurun_out/bench_win.json
+timeout 600 python bench.py --kind windowed --dtype f32 --no-cpu-baseline --compare "" > gpurun_out/bench_win32.json 2>> gpurun_out/bench.err; echo "bench win32 rc=$?"; cat gpurun_out/bench_win32.json
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_windowed -c 1 -o gpurun_out/ncu_win_c5 python tools/prof_one.py c5 windowed 3 > gpurun_out/ncu_win.log 2>&1; echo "ncu rc=$?"; tail -1 gpurun_out/ncu_win.log
