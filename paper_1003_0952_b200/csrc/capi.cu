@@ -715,7 +715,12 @@ void* gather_stage_fn_M(int pf) {
 
 template <class T, int L, int U, int NB>
 void* gather_stage_fn_NB(int pf, int minb) {
-    return minb == 8 ? gather_stage_fn_M<T, L, U, NB, 8>(pf) : gather_stage_fn_M<T, L, U, NB, 1>(pf);
+    switch (minb) {
+        case 8: return gather_stage_fn_M<T, L, U, NB, 8>(pf);
+        case 6: return gather_stage_fn_M<T, L, U, NB, 6>(pf);
+        case 5: return gather_stage_fn_M<T, L, U, NB, 5>(pf);
+        default: return gather_stage_fn_M<T, L, U, NB, 1>(pf);
+    }
 }
 
 template <class T, int L>
@@ -993,7 +998,10 @@ void setup_gather(Plan& P, const MatView& a) {
     P.gather_u = env_int("CSRC_GPU_GU", avg / P.gather_lanes <= 16 ? 8 : 4) == 8 ? 8 : 4;
     P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
     P.gather_nt = env_int("CSRC_GPU_GNT", 256) == 128 ? 128 : 256;
-    P.gather_minb = env_int("CSRC_GPU_GMINB", 1) == 8 ? 8 : 1;
+    {
+        const int mb = env_int("CSRC_GPU_GMINB", 1);
+        P.gather_minb = (mb == 8 || mb == 6 || mb == 5) ? mb : 1;
+    }
     std::vector<int32_t> pbase, pat_off;
     const bool has_pat = P.gather_lanes <= 8 && find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns);
     P.gather_pat = has_pat && env_int("CSRC_GPU_GPATTERN", 1) != 0 ? 1 : 0;
