@@ -5,14 +5,18 @@
 // windows, colour classes, private buffers) and a stream; apply() enqueues
 // init / compute / accumulate phases and records PhaseTimings-style events.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <unordered_map>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "hostlink.cuh"
 #include "internal.hpp"
 #include "kernels.cuh"
 
@@ -51,7 +55,23 @@ struct DevBuf {
 template <class U>
 void upload(DevBuf& d, const U* h, size_t count) {
     d.alloc(count * sizeof(U));
-    if (count) CUDA_OK(cudaMemcpy(d.p, h, count * sizeof(U), cudaMemcpyHostToDevice));
+    if (!count) return;
+    const size_t bytes = count * sizeof(U);
+    if (bytes < (size_t(64) << 20)) {
+        CUDA_OK(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
+        return;
+    }
+    // large plan arrays: pinned staging + parallel memcpy (hostlink.cuh)
+    cudaStream_t st = nullptr;
+    CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    try {
+        HostLink hl(st);
+        hl.h2d(d.p, h, bytes);
+    } catch (...) {
+        cudaStreamDestroy(st);
+        throw;
+    }
+    cudaStreamDestroy(st);
 }
 
 int pow2_at_least(int64_t v) {
@@ -217,6 +237,22 @@ void upload_values(DevBuf& d, const double* h, size_t count) {
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);  // tuning knobs for sweeps
     return e ? std::atoi(e) : dflt;
+}
+
+// Host plan building over T threads: f(t, begin, end) on contiguous slices
+// of [0, count). Plans for large matrices walk hundreds of millions of pairs.
+template <class F>
+void parallel_slices(int64_t count, F&& f, int64_t grain = 65536) {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int T = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(std::min(hw, 32), count / grain)));
+    if (T <= 1) {
+        f(0, int64_t{0}, count);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t)
+        pool.emplace_back([&, t] { f(t, count * t / T, count * (t + 1) / T); });
+    for (auto& th : pool) th.join();
 }
 
 // Shared-memory rings for the windowed kernel's scatters (CSRC_GPU_WIN_RINGS=1).
@@ -658,14 +694,24 @@ int grid_for(int device, int64_t work, int per_block);
 // order); pbase[q] = start of row q's pattern in pat_off. Gives up (returns
 // false) past 65535 patterns or 1 M stored offsets: then the plan keeps
 // explicit column indices.
-bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const std::vector<int32_t>& eidx,
+bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const HVec<int32_t>& eidx,
                        std::vector<int32_t>& pbase, std::vector<int32_t>& pat_off, int32_t* n_patterns) {
     pbase.assign(static_cast<size_t>(n), 0);
     pat_off.clear();
     std::vector<int32_t> pat_ptr(1, 0);
     std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+    int32_t prev = -1;  // consecutive rows usually share a pattern: try it first
     for (index_t q = 0; q < n; ++q) {
         const int32_t e0 = eptr[q], len = eptr[q + 1] - e0;
+        if (prev >= 0 && pat_ptr[prev + 1] - pat_ptr[prev] == len) {
+            const int32_t p0 = pat_ptr[prev];
+            bool same = true;
+            for (int32_t j = 0; j < len && same; ++j) same = pat_off[p0 + j] == eidx[e0 + j] - q;
+            if (same) {
+                pbase[q] = p0;
+                continue;
+            }
+        }
         uint64_t h = 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(len);
         for (int32_t j = 0; j < len; ++j)
             h = (h ^ static_cast<uint32_t>(eidx[e0 + j] - q)) * 0x100000001B3ull;
@@ -689,6 +735,7 @@ bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const std::v
             cand.push_back(found);
         }
         pbase[q] = pat_ptr[found];
+        prev = found;
     }
     *n_patterns = static_cast<int32_t>(pat_ptr.size()) - 1;
     if (pat_off.empty()) pat_off.push_back(0);  // keep the device table non-empty
@@ -818,8 +865,8 @@ void* sell_fn(const Plan& P) {
 // slots; entry j of local row rl at sbase[s] + 32 (j / L) + L rl + j % L;
 // padding slots hold zeros and are never read.
 template <class T>
-void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const std::vector<int32_t>& eidx,
-                const std::vector<double>& ev, const std::vector<double>& evt, bool value_symmetric,
+void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const HVec<int32_t>& eidx,
+                const HVec<double>& ev, const HVec<double>& evt, bool value_symmetric,
                 const std::vector<int32_t>& pbase, const std::vector<int32_t>& pat_off) {
     const double avg = n ? static_cast<double>(eptr[n]) / n : 0.0;
     // lanes per row: rows of <= 40 entries (27-point stencils) split over 2
@@ -845,21 +892,24 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const std:
     const size_t tot = static_cast<size_t>(sbase[ns]);
     P.sell_entries = static_cast<int64_t>(tot);
     std::vector<int32_t> rmeta(static_cast<size_t>(n));
-    std::vector<int32_t> sidx(pat ? 0 : tot, 0);
-    std::vector<double> sv(tot, 0.0), svt(value_symmetric ? 0 : tot, 0.0);
+    // padding slots are never read: no value-initialisation (parallel first touch)
+    HVec<int32_t> sidx(pat ? 0 : tot);
+    HVec<double> sv(tot), svt(value_symmetric ? 0 : tot);
     const int Ln = P.sell_lanes;
-    for (int64_t sl = 0; sl < ns; ++sl)
-        for (int64_t r = sl * H; r < std::min<int64_t>(n, sl * H + H); ++r) {
-            const int32_t len = eptr[r + 1] - eptr[r];
-            rmeta[r] = pat ? (pbase[r] | (len << 20)) : len;
-            const size_t b = static_cast<size_t>(sbase[sl]) + static_cast<size_t>(Ln * (r - sl * H));
-            for (int32_t j = 0; j < len; ++j) {
-                const size_t d = b + 32 * static_cast<size_t>(j / Ln) + static_cast<size_t>(j % Ln);
-                sv[d] = ev[eptr[r] + j];
-                if (!value_symmetric) svt[d] = evt[eptr[r] + j];
-                if (!pat) sidx[d] = eidx[eptr[r] + j];
+    parallel_slices(ns, [&](int, int64_t s0, int64_t s1) {
+        for (int64_t sl = s0; sl < s1; ++sl)
+            for (int64_t r = sl * H; r < std::min<int64_t>(n, sl * H + H); ++r) {
+                const int32_t len = eptr[r + 1] - eptr[r];
+                rmeta[r] = pat ? (pbase[r] | (len << 20)) : len;
+                const size_t b = static_cast<size_t>(sbase[sl]) + static_cast<size_t>(Ln * (r - sl * H));
+                for (int32_t j = 0; j < len; ++j) {
+                    const size_t d = b + 32 * static_cast<size_t>(j / Ln) + static_cast<size_t>(j % Ln);
+                    sv[d] = ev[eptr[r] + j];
+                    if (!value_symmetric) svt[d] = evt[eptr[r] + j];
+                    if (!pat) sidx[d] = eidx[eptr[r] + j];
+                }
             }
-        }
+    }, 1024);
     upload(P.sbase, sbase.data(), sbase.size());
     upload(P.rmeta, rmeta.data(), rmeta.size());
     upload_values<T>(P.sval, sv.data(), sv.size());
@@ -894,55 +944,103 @@ void setup_gather(Plan& P, const MatView& a) {
     const bool band = n != N;
     if (2 * static_cast<int64_t>(a.k) > INT32_MAX)
         throw Error("gather plan: more than 2^31 off-diagonal entries (use the windowed kernel)");
+    // CSRC_GPU_PLAN_TRACE=1: phase times of the plan build on stderr (diagnostics)
+    const bool trace = env_int("CSRC_GPU_PLAN_TRACE", 0) != 0;
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "gather plan: %-22s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
+    // upper entries of q = the pairs (r, q), r > q: count them per column
+    // (relaxed atomic increments) and find x_hi, over row slices in parallel
     std::vector<int32_t> up(static_cast<size_t>(n) + 1, 0);
+    std::vector<index_t> xhi_t(64, r1);
+    parallel_slices(N - (r0 + 1), [&](int t, int64_t b, int64_t e) {
+        index_t xh = r1;
+        for (index_t r = static_cast<index_t>(r0 + 1 + b); r < r0 + 1 + e; ++r)
+            for (index_t q = a.ia[r]; q < a.ia[r + 1]; ++q)
+                if (a.ja[q] >= r0 && a.ja[q] < r1) {
+                    __atomic_fetch_add(&up[a.ja[q] - r0 + 1], 1, __ATOMIC_RELAXED);
+                    xh = std::max(xh, r + 1);
+                }
+        xhi_t[t] = xh;
+    });
     index_t x_hi = r1;
-    for (index_t r = r0 + 1; r < N; ++r)
-        for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t)
-            if (a.ja[t] >= r0 && a.ja[t] < r1) {
-                ++up[a.ja[t] - r0 + 1];
-                x_hi = std::max(x_hi, r + 1);
-            }
+    for (index_t v : xhi_t) x_hi = std::max(x_hi, v);
     P.x_hi = x_hi;
+    mark("upper counts");
     std::vector<int32_t> eptr(static_cast<size_t>(n) + 1, 0);
     for (index_t q = 0; q < n; ++q)
         eptr[q + 1] = eptr[q] + (a.ia[r0 + q + 1] - a.ia[r0 + q]) + up[q + 1];
     const size_t ne = static_cast<size_t>(eptr[n]);
-    std::vector<int32_t> eidx(ne);
-    std::vector<double> ev(ne), evt(a.value_symmetric ? 0 : ne);
+    // no value-initialisation: every slot is written below, and the first-touch
+    // page faults of these multi-GB arrays happen in the parallel fill
+    HVec<int32_t> eidx(ne);
+    HVec<double> ev(ne), evt(a.value_symmetric ? 0 : ne);
     std::vector<int32_t> next(static_cast<size_t>(n));
-    for (index_t q = 0; q < n; ++q) {
-        int32_t w = eptr[q];
-        for (index_t t = a.ia[r0 + q]; t < a.ia[r0 + q + 1]; ++t, ++w) {
-            eidx[w] = a.ja[t] - r0;
-            ev[w] = a.al[t];
-            if (!a.value_symmetric) evt[w] = a.au[t];
+    parallel_slices(n, [&](int, int64_t b, int64_t e) {  // lower pairs, row by row
+        for (index_t q = static_cast<index_t>(b); q < e; ++q) {
+            int32_t w = eptr[q];
+            for (index_t t = a.ia[r0 + q]; t < a.ia[r0 + q + 1]; ++t, ++w) {
+                eidx[w] = a.ja[t] - r0;
+                ev[w] = a.al[t];
+                if (!a.value_symmetric) evt[w] = a.au[t];
+            }
+            next[q] = w;  // upper entries of q start here
         }
-        next[q] = w;  // upper entries of q start here
-    }
-    for (index_t r = r0 + 1; r < N; ++r)  // ascending r: upper entries land sorted
-        for (index_t t = a.ia[r]; t < a.ia[r + 1]; ++t) {
-            if (a.ja[t] < r0 || a.ja[t] >= r1) continue;
-            const int32_t w = next[a.ja[t] - r0]++;
-            eidx[w] = r - r0;
-            ev[w] = a.value_symmetric ? a.al[t] : a.au[t];
-            if (!a.value_symmetric) evt[w] = a.al[t];
+    });
+    mark("alloc + lower pairs");
+    // upper pairs: thread t owns the target rows (columns) [qb, qe) and walks the
+    // rows r > qb in ascending order, so each target's upper entries land
+    // sorted by r -- the same order as a serial pass, whatever the thread count.
+    // Rows whose smallest column (ja ascends within a row) is >= the slice end
+    // cannot name one of its targets.
+    parallel_slices(n, [&](int, int64_t qb, int64_t qe) {
+        const index_t lo_col = static_cast<index_t>(r0 + qb), hi_col = static_cast<index_t>(r0 + qe);
+        int64_t remaining = 0;  // upper entries of the slice still to place: stop at 0
+        for (int64_t q = qb; q < qe; ++q) remaining += up[q + 1];
+        for (index_t r = std::max<index_t>(r0 + 1, lo_col + 1); r < N && remaining > 0; ++r) {
+            const index_t t0 = a.ia[r], t1 = a.ia[r + 1];
+            if (t0 == t1 || a.ja[t0] >= hi_col) continue;
+            for (index_t t = t0; t < t1; ++t) {
+                const index_t c = a.ja[t];
+                if (c < lo_col) continue;
+                if (c >= hi_col) break;
+                const int32_t w = next[c - r0]++;
+                eidx[w] = r - r0;
+                ev[w] = a.value_symmetric ? a.al[t] : a.au[t];
+                if (!a.value_symmetric) evt[w] = a.al[t];
+                --remaining;
+            }
         }
+    });
+    mark("upper pairs");
     {
         // interior rows of a band: all columns inside the band's own rows [0, n)
+        std::vector<index_t> b0_t(64, 0), b1_t(64, n);
+        parallel_slices(n, [&](int t, int64_t qb, int64_t qe) {
+            index_t lo = 0, hi = n;
+            for (index_t q = static_cast<index_t>(qb); q < qe; ++q)
+                for (int32_t e = eptr[q]; e < eptr[q + 1]; ++e) {
+                    if (eidx[e] < 0) lo = std::max(lo, q + 1);
+                    if (eidx[e] >= n) hi = std::min(hi, q);
+                }
+            b0_t[t] = lo;
+            b1_t[t] = hi;
+        });
         index_t b0 = 0, b1 = n;
-        for (index_t q = 0; q < n; ++q)
-            for (int32_t e = eptr[q]; e < eptr[q + 1]; ++e) {
-                if (eidx[e] < 0) b0 = std::max(b0, q + 1);
-                if (eidx[e] >= n) b1 = std::min(b1, q);
-            }
+        for (int t = 0; t < 64; ++t) {
+            b0 = std::max(b0, b0_t[t]);
+            b1 = std::min(b1, b1_t[t]);
+        }
         const index_t a0 = (b0 + 255) / 256 * 256, a1 = b1 == n ? n : b1 / 256 * 256;
         P.gi0 = std::min(a0, n);
         P.gi1 = std::max(P.gi0, a1);
     }
-    upload(P.eptr, eptr.data(), eptr.size());
-    upload_values<T>(P.eval, ev.data(), ev.size());
-    if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
-
+    mark("interior split");
     const double avg = n ? static_cast<double>(ne) / n : 0.0;
     P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? 2 : avg <= 128 ? 4 : 8);
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
@@ -984,13 +1082,16 @@ void setup_gather(Plan& P, const MatView& a) {
         if (P.hchunk.back() != n) P.hchunk.push_back(n);
         const int nc = static_cast<int>(P.hchunk.size()) - 1;
         P.hneed.assign(nc, 0);
-        for (int c = 0; c < nc; ++c) {
-            int32_t hi = P.hchunk[c + 1] - 1;  // the diagonal reads x[row]
-            for (int64_t e = eptr[P.hchunk[c]]; e < eptr[P.hchunk[c + 1]]; ++e) hi = std::max(hi, eidx[e]);
-            // chunk holding column hi
-            P.hneed[c] = static_cast<int32_t>(std::upper_bound(P.hchunk.begin(), P.hchunk.end() - 1, hi) -
-                                              P.hchunk.begin()) - 1;
-        }
+        std::vector<std::thread> pool;
+        for (int c = 0; c < nc; ++c)
+            pool.emplace_back([&, c] {
+                int32_t hi = P.hchunk[c + 1] - 1;  // the diagonal reads x[row]
+                for (int64_t e = eptr[P.hchunk[c]]; e < eptr[P.hchunk[c + 1]]; ++e) hi = std::max(hi, eidx[e]);
+                // chunk holding column hi
+                P.hneed[c] = static_cast<int32_t>(std::upper_bound(P.hchunk.begin(), P.hchunk.end() - 1, hi) -
+                                                  P.hchunk.begin()) - 1;
+            });
+        for (auto& th : pool) th.join();
     }
     // staged form (k_gather_staged): U x-gathers in flight per lane, NB buffers,
     // NT threads per block; the row-pattern form when the rows repeat a small
@@ -1002,8 +1103,10 @@ void setup_gather(Plan& P, const MatView& a) {
         const int mb = env_int("CSRC_GPU_GMINB", 1);
         P.gather_minb = (mb == 8 || mb == 6 || mb == 5) ? mb : 1;
     }
+    mark("host pipeline chunks");
     std::vector<int32_t> pbase, pat_off;
     const bool has_pat = P.gather_lanes <= 8 && find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns);
+    mark("row patterns");
     P.gather_pat = has_pat && env_int("CSRC_GPU_GPATTERN", 1) != 0 ? 1 : 0;
     if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 2 && P.gather_lanes <= 8) {
         const int R = P.gather_nt / P.gather_lanes;
@@ -1038,10 +1141,16 @@ void setup_gather(Plan& P, const MatView& a) {
     // columns (C3) -- profiles/r01_sweep_sell3.txt. CSRC_GPU_GSELL=0/1 forces.
     const int sell_env = env_int("CSRC_GPU_GSELL", -1);
     const bool sell_auto = has_pat && avg > 40.0;  // (not P.gather_pat: explicit columns keep the same form)
+    mark("staged-kernel config");
     if ((sell_env == 1 || (sell_env < 0 && sell_auto)) && n > 0) {
         setup_sell<T>(P, n, eptr, eidx, ev, evt, a.value_symmetric, pbase, pat_off);
+        mark("sliced layout + upload");
         return;
     }
+    upload(P.eptr, eptr.data(), eptr.size());
+    upload_values<T>(P.eval, ev.data(), ev.size());
+    if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
+    mark("value uploads");
     if (!P.gather_buf) P.gather_pat = 0;  // the plain row kernel reads explicit indices
     if (P.gather_pat) {
         upload(P.pbase, pbase.data(), pbase.size());
