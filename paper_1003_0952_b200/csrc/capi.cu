@@ -1098,7 +1098,13 @@ void setup_gather(Plan& P, const MatView& a) {
     // dictionary of column-offset patterns
     P.gather_u = env_int("CSRC_GPU_GU", avg / P.gather_lanes <= 16 ? 8 : 4) == 8 ? 8 : 4;
     P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
-    P.gather_nt = env_int("CSRC_GPU_GNT", 256) == 128 ? 128 : 256;
+    {
+        // 128-thread blocks (64 rows) for fp64: C5 0.631 ms vs 0.689 ms at 256 and
+        // 0.664 at 64; fp32 keeps 256 (0.466 vs 0.558 ms)
+        // (profiles/r01_sweep_gather_block_threads{,_64}.txt)
+        const int nt = env_int("CSRC_GPU_GNT", sizeof(T) == 8 ? 128 : 256);
+        P.gather_nt = (nt == 64 || nt == 128) ? nt : 256;
+    }
     {
         const int mb = env_int("CSRC_GPU_GMINB", 1);
         P.gather_minb = (mb == 8 || mb == 6 || mb == 5) ? mb : 1;

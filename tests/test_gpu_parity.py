@@ -403,6 +403,10 @@ GATHER_SHAPES = [
     {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_U": "9"},
     {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_U": "14", "CSRC_GPU_SELL_L": "2"},
     {"CSRC_GPU_GSELL": "0"},
+    # staged block sizes: 256 (the fp32 default), 128 (fp64 default), 64 threads
+    {"CSRC_GPU_GNT": "256"},
+    {"CSRC_GPU_GNT": "64"},
+    {"CSRC_GPU_GNT": "128", "CSRC_GPU_GPATTERN": "0"},
 ]
 
 
