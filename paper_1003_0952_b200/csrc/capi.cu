@@ -587,6 +587,7 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.far_hi = P.far_hi;
     A.ring_near = P.ring_near;
     A.ring_far = P.ring_far;
+    A.rotate = env_int("CSRC_GPU_WIN_ROTATE", 0);  // diagnostics (see windowed.cuh)
     A.max_tile_pairs = P.max_tile_pairs;
     A.stages = P.stages;
     A.stage_bytes = P.stage_bytes;

@@ -79,6 +79,7 @@ struct WinArgs {
     int32_t max_tile_pairs;
     int32_t stages;             // TMA pipeline depth
     int32_t stage_bytes;
+    int32_t rotate;             // batch-order rotation period (0/1: none)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -381,7 +382,12 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
             const uint32_t ja_b = ja_b0 + 4u * first;
             const uint32_t al_b = al_b0 + E * first;
             const uint32_t au_b = au_b0 + E * first;
-            for (int32_t bt = 0; bt < nb; ++bt) {
+            // rotated batch order (A.rotate): consecutive rows start on different
+            // batches, so rows sharing their column lists (3x3 dof blocks) do not
+            // hit the same scatter targets at the same time
+            const int32_t rot = A.rotate > 1 && nb > 1 ? (g % A.rotate) % nb : 0;
+            for (int32_t bi = 0; bi < nb; ++bi) {
+                const int32_t bt = bi + rot < nb ? bi + rot : bi + rot - nb;
                 int32_t mm[4], j[4];
                 T xv[4];
 #pragma unroll
