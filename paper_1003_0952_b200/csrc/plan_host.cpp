@@ -37,12 +37,42 @@ MatView view_of(const csrc_host_matrix* a, bool check_structure) {
                     std::to_string(v.k));
     if (check_structure && v.n > 0) {
         if (v.ia[0] != 0) throw Error("matrix: ia[0] must be 0");
-        for (index_t i = 0; i < v.n; ++i) {
-            if (v.ia[i + 1] < v.ia[i]) throw Error("matrix: ia not nondecreasing at row " +
-                                                   std::to_string(i));
+        // rows checked over threads; the first offending row (lowest index) is
+        // reported, as a serial scan would
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        const int T = static_cast<int>(std::max<count_t>(1, std::min<count_t>(std::min(hw, 32), v.n / 65536)));
+        std::vector<index_t> bad(static_cast<size_t>(T), v.n);
+        auto check = [&](int th) {
+            const index_t b = static_cast<index_t>(static_cast<count_t>(v.n) * th / T);
+            const index_t e = static_cast<index_t>(static_cast<count_t>(v.n) * (th + 1) / T);
+            for (index_t i = b; i < e; ++i) {
+                bool ok = v.ia[i + 1] >= v.ia[i];
+                index_t prev = -1;
+                for (index_t t = v.ia[i]; ok && t < v.ia[i + 1]; ++t) {
+                    const index_t j = v.ja[t];
+                    ok = !(j <= prev || j >= i || j < 0);
+                    prev = j;
+                }
+                if (!ok) {
+                    bad[th] = i;
+                    return;
+                }
+            }
+        };
+        if (T == 1) {
+            check(0);
+        } else {
+            std::vector<std::thread> pool;
+            for (int th = 0; th < T; ++th) pool.emplace_back(check, th);
+            for (auto& t : pool) t.join();
+        }
+        const index_t i = *std::min_element(bad.begin(), bad.end());
+        if (i < v.n) {
+            if (v.ia[i + 1] < v.ia[i])
+                throw Error("matrix: ia not nondecreasing at row " + std::to_string(i));
             index_t prev = -1;
             for (index_t t = v.ia[i]; t < v.ia[i + 1]; ++t) {
-                index_t j = v.ja[t];
+                const index_t j = v.ja[t];
                 if (j <= prev || j >= i || j < 0)
                     throw Error("matrix: row " + std::to_string(i) +
                                 " lower columns must be strictly increasing and < row (ja[" +
