@@ -14,9 +14,17 @@ import paper_1003_0952_b200 as P  # noqa: E402
 a, x, _ = P.config_matrix("c5")
 xd = torch.from_numpy(x).cuda()
 yd = torch.zeros_like(xd)
-for nt in sys.argv[1].split(","):
-    os.environ["CSRC_GPU_GNT"] = nt
-    ex = P.GpuSpmv(a, P.Strategy(P.StrategyKind.gather))
+# each argument: "KIND:ENV=V;ENV=V" (KIND gather|windowed), or a bare staged block size
+for spec in sys.argv[1].split(","):
+    kind, _, envs = spec.partition(":") if ":" in spec else ("gather", "", f"CSRC_GPU_GNT={spec}")
+    saved = dict(os.environ)
+    for kv in filter(None, envs.split(";")):
+        k, v = kv.split("=")
+        os.environ[k] = v
+    ex = P.GpuSpmv(a, P.Strategy(P.StrategyKind[kind]))
+    os.environ.clear()
+    os.environ.update(saved)
+    nt = spec
     for _ in range(10):
         ex.apply_device(xd, yd)
     tot, ker = ex.time_products(xd, yd, 400, 0)
