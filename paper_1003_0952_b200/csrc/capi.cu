@@ -1365,7 +1365,13 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
 
 Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const CreateOpts& o) {
     if (!s) throw Error("null strategy");
+    const bool trace = env_int("CSRC_GPU_PLAN_TRACE", 0) != 0;
+    const auto t_start = std::chrono::steady_clock::now();
+    auto since = [&] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    };
     MatView a = view_of(m, true);
+    if (trace) std::fprintf(stderr, "plan: structure check           %8.1f ms\n", since());
     // ParallelSpmv ctor checks (parallel.hpp:229-234)
     if (s->p < 1) throw Error("ParallelSpmv: thread count must be >= 1");
     if (s->kind == CSRC_KIND_SEQUENTIAL && s->p != 1)
@@ -1444,10 +1450,12 @@ Plan* create_plan(const csrc_host_matrix* m, const csrc_gpu_strategy* s, const C
     CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
     for (auto& e : P->ev) CUDA_OK(cudaEventCreate(&e));
     if (a.n == 0) return P.release();
+    if (trace) std::fprintf(stderr, "plan: streams + events          %8.1f ms\n", since());
     if (P->dtype == CSRC_DTYPE_F64)
         create_typed<double>(*P, a, *s, o);
     else
         create_typed<float>(*P, a, *s, o);
+    if (trace) std::fprintf(stderr, "plan: total in the library      %8.1f ms\n", since());
     return P.release();
 }
 
