@@ -8,15 +8,16 @@
 // scatter, no atomics, no memset: each y element is written exactly once
 // with a fixed summation order (bit-reproducible).
 //
-// k_gather_rows: L lanes per row, grid-stride over row blocks. At full
-// occupancy (<= 32 registers) the loads one warp keeps in flight are too few
-// to cover HBM latency (Little's law: ~49 KB per SM at 64 warps), so thread 0
-// of each block issues a TMA bulk L2 prefetch (cp.async.bulk.prefetch.L2,
-// no registers, no shared memory) of the eidx / eval spans the block will
-// read PF iterations later; the demand loads then hit L2.
-// (A warp-specialised variant that staged row tiles in shared memory and
-// walked them one row per lane lost 1.2-6x: shared memory holds ~700 rows,
-// too few independent x gathers per SM; profiles/r01_sweep_gather_staged.txt.)
+// Three kernel forms (capi.cu setup_gather picks one per plan):
+//   k_gather_staged  the default: a row block's value span (and explicit
+//                    columns) staged in shared memory by one TMA bulk copy;
+//                    row-pattern compression of the columns (PF = 1)
+//   k_gather_sell    SELL-sliced layout, one warp per slice, loads in flight
+//                    from registers; chosen for long patterned rows (C4)
+//   k_gather_rows    plain L-lanes-per-row fallback for rows whose entry
+//                    span does not fit a staging buffer (optional TMA L2
+//                    prefetch of future spans, off by default: it hurt)
+// Measured alternatives that lost are recorded in DESIGN.md §5.
 #pragma once
 
 #include <cstdint>
