@@ -218,6 +218,36 @@ def test_edge_cases():
         assert rel_l2(run(a, x, s), O.spmv_csrc(a, x)) <= TOL64, name
 
 
+@pytest.mark.parametrize("env", [{}, {"CSRC_GPU_GSELL": "1"}, {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_L": "2"},
+                                 {"CSRC_GPU_GNT": "256"}])
+def test_non_finite_x_and_ragged_sizes(env, monkeypatch):
+    """inf / NaN in x propagate to exactly the rows the oracle marks (no
+    padding or out-of-row slot is ever multiplied in), on sizes that are not
+    multiples of a slice, a row block or a tile."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(11)
+    for n in (1, 31, 33, 257, 1000):
+        m = meshes().matrix("g1_")
+        if n > m.n:
+            continue
+        # leading principal n x n block of a mesh matrix (rows keep their lower pairs < n)
+        ia = m.ia[: n + 1].copy()
+        k = int(ia[n])
+        a = P.CsrcMatrix(n, m.ad[:n], ia, m.ja[:k], m.al[:k], m.au[:k])
+        x = rng.uniform(-1, 1, n)
+        x[n // 2] = np.inf
+        if n > 2:
+            x[n // 3] = np.nan
+        ref = O.spmv_csrc(a, x)
+        for kind in (K.gather, K.windowed, K.atomic, K.colorful):
+            y = run(a, x, P.Strategy(kind, p=2 if kind == K.colorful else 1))
+            assert np.array_equal(np.isnan(y), np.isnan(ref)), (n, kind)
+            assert np.array_equal(np.isinf(y), np.isinf(ref)), (n, kind)
+            fin = np.isfinite(ref)
+            assert rel_l2(y[fin], ref[fin]) <= TOL64
+
+
 def test_device_and_graph_entry_points():
     import torch
     a, x, _ = P.config_matrix("c1")
