@@ -141,6 +141,7 @@ typedef struct {
     int64_t rect_nnz;           /* rectangular plans: entries of the CSR tail        */
     int32_t gather_form;        /* gather plans: 1 k_gather_rows, 2 k_gather_staged,
                                    3 k_gather_sell; 0 for the other kinds            */
+    int32_t csr_cols;           /* CSR plans: columns of A (x length); 0 otherwise  */
 } csrc_gpu_plan_info;
 
 typedef struct csrc_gpu_plan_s* csrc_gpu_plan_t;
@@ -178,6 +179,14 @@ int csrc_gpu_plan_create_partitioned(const csrc_host_matrix* a, const csrc_gpu_s
  * (still missing the halo partials of higher bands). */
 int csrc_gpu_plan_create_band(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                               int32_t row_begin, int32_t row_end, csrc_gpu_plan_t* out);
+
+/* spmv_csr (kernels.hpp:7-22) on the GPU: a plan over a general CSR matrix
+ * (n_rows x n_cols, any pattern, csr.hpp:28-51), run by the gather kernels on
+ * the rows as they stand; strategy kind SEQUENTIAL or GATHER. x has n_cols
+ * entries, y n_rows; no transpose product. The reference's Format::csr
+ * baseline of the CSRC-vs-CSR comparison (bench.hpp:203-215). */
+int csrc_gpu_plan_create_csr(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, const int32_t* col_idx,
+                             const double* values, const csrc_gpu_strategy* s, csrc_gpu_plan_t* out);
 
 /* ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181) and
  * spmv_csrc_rect (kernels.hpp:69-91): the n x n CSRC part `a` plus the CSR

@@ -228,6 +228,26 @@ std::pair<Vector, PhaseTimings> spmv_parallel(const M& a, const Vector& x, const
     return {std::move(y), ex.last_timings()};
 }
 
+/// spmv_csr (kernels.hpp:7-22) on the GPU: any CsrMatrix-shaped type
+/// (n_rows, n_cols, row_ptr, col_idx, values).
+template <class M>
+Vector spmv_csr(const M& a, const Vector& x) {
+    if (static_cast<long long>(x.size()) != static_cast<long long>(a.n_cols))
+        throw Error("spmv_csr: x has length " + std::to_string(x.size()) + ", expected " +
+                    std::to_string(a.n_cols));
+    std::vector<int32_t> rp(a.row_ptr.begin(), a.row_ptr.end());
+    std::vector<int32_t> ci(a.col_idx.begin(), a.col_idx.end());
+    const csrc_gpu_strategy st = Strategy().c();
+    csrc_gpu_plan_t plan = nullptr;
+    check(csrc_gpu_plan_create_csr(static_cast<int32_t>(a.n_rows), static_cast<int32_t>(a.n_cols), rp.data(),
+                                   ci.data(), a.values.data(), &st, &plan));
+    Vector y(static_cast<size_t>(a.n_rows));
+    const int rc = csrc_gpu_spmv(plan, x.data(), static_cast<int64_t>(x.size()), y.data());
+    csrc_gpu_plan_destroy(plan);
+    check(rc);
+    return y;
+}
+
 /// spmv_csrc_rect (kernels.hpp:69-91) on the GPU: x has r.m entries.
 template <class R>
 Vector spmv_csrc_rect(const R& r, const Vector& x) {

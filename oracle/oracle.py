@@ -310,6 +310,17 @@ class Ref:
                                               _p(ci, C.c_int32), _p(va, C.c_double)))
         return self._built_out(), self._csr_out()
 
+    def spmv_csr(self, n_rows, n_cols, rp, ci, va, x):
+        """spmv_csr (kernels.hpp:7-22) of the reference itself."""
+        rp = np.ascontiguousarray(rp, np.int32)
+        ci = np.ascontiguousarray(ci, np.int32)
+        va = np.ascontiguousarray(va, np.float64)
+        x = np.ascontiguousarray(x, np.float64)
+        y = np.zeros(max(n_rows, 1), np.float64)
+        self._chk(self.lib.ref_spmv_csr(C.c_int32(n_rows), C.c_int32(n_cols), _p(rp, C.c_int32), _p(ci, C.c_int32),
+                                        _p(va, C.c_double), _p(x, C.c_double), _p(y, C.c_double)))
+        return y[:n_rows]
+
     def spmv_csrc_rect(self, r, x):
         """spmv_csrc_rect (kernels.hpp:69-91) of the reference itself."""
         a, t = r.square, r.rect

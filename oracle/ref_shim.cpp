@@ -112,6 +112,22 @@ void ref_csr_copy(int32_t* rp, int32_t* ci, double* va) {
     std::memcpy(va, g_csr.values.data(), sizeof(double) * g_csr.values.size());
 }
 
+// spmv_csr (kernels.hpp:7-22) of the reference.
+int ref_spmv_csr(int32_t n_rows, int32_t n_cols, const int32_t* rp, const int32_t* ci, const double* va,
+                 const double* x, double* y) {
+    return guarded([&] {
+        CsrMatrix a;
+        a.n_rows = n_rows;
+        a.n_cols = n_cols;
+        a.row_ptr.assign(rp, rp + n_rows + 1);
+        a.col_idx.assign(ci, ci + rp[n_rows]);
+        a.values.assign(va, va + rp[n_rows]);
+        Vector xv(x, x + n_cols);
+        Vector out = spmv_csr(a, xv);
+        std::memcpy(y, out.data(), sizeof(double) * n_rows);
+    });
+}
+
 // decompose_rect (csrc_matrix.hpp:113-142): square part -> ref_built_*, tail -> ref_csr_*.
 int ref_decompose_rect(int32_t n_rows, int32_t n_cols, const int32_t* rp, const int32_t* ci,
                        const double* va) {

@@ -26,6 +26,7 @@ reference (file:line)                  here
 ``csr_to_csrc`` csrc_matrix.hpp:44-91    :func:`csr_to_csrc`, :func:`build_csrc`
 ``decompose_rect`` csrc_matrix.hpp:113   :func:`decompose_rect`
 ``spmv_csrc_rect`` kernels.hpp:69-91     :func:`spmv_csrc_rect`; ``GpuSpmv(CsrcRectMatrix, s)``
+``spmv_csr`` kernels.hpp:7-22            :func:`spmv_csr`; ``GpuSpmv(CsrMatrix, s)``
 =====================================  =============================================
 
 Errors raise :class:`Error` (``csrc::Error``, common.hpp:15-18) with the
@@ -51,7 +52,7 @@ __all__ = [
     "conflict_edge_counts", "ColorfulPlan", "LocalBuffersPlan", "working_set_kb",
     "model_bytes", "model_flops", "Mesh", "generate_fixture", "CONFIGS", "config_matrix",
     "fixture_u01", "TripletMatrix", "CsrMatrix", "CsrcRectMatrix", "build_csr", "build_csrc",
-    "csr_to_csrc", "decompose_rect", "csrc_to_triplets", "spmv_csrc_rect",
+    "csr_to_csrc", "decompose_rect", "csrc_to_triplets", "spmv_csrc_rect", "spmv_csr",
 ]
 
 
@@ -384,6 +385,22 @@ class GpuSpmv:
 
     def __init__(self, a, strategy: Strategy = Strategy(), plan=None,
                  band: Optional[Tuple[int, int]] = None):
+        if isinstance(a, CsrMatrix):
+            # spmv_csr (kernels.hpp:7-22): a plan over a general CSR matrix
+            if plan is not None or band is not None:
+                raise Error("CSR plans take no explicit plan or band")
+            self._a_n = int(a.n_rows)
+            self.strategy = strategy
+            self._h = C.c_void_p()
+            rp = _as(a.row_ptr, np.int32)
+            ci = _as(a.col_idx, np.int32)
+            va = _as(a.values, np.float64)
+            s = strategy._c()
+            _check(L.plan_create_csr(int(a.n_rows), int(a.n_cols), rp.ctypes.data_as(L.P_i32),
+                                     ci.ctypes.data_as(L.P_i32) if ci.size else None,
+                                     va.ctypes.data_as(L.P_f64) if va.size else None, C.byref(s), C.byref(self._h)))
+            self._timings = PhaseTimings()
+            return
         rect = a if isinstance(a, CsrcRectMatrix) else None
         if rect is not None:
             a = rect.square
@@ -542,6 +559,18 @@ def spmv_csrc(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarray:
     xv = _as(x, np.float64)
     if xv.size != a.n:
         raise Error(f"spmv_csrc: x has length {xv.size}, expected {a.n}")
+    ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype))
+    try:
+        return ex.apply(xv)
+    finally:
+        ex.close()
+
+
+def spmv_csr(a, x, dtype: DType = DType.f64) -> np.ndarray:
+    """spmv_csr (kernels.hpp:7-22) on the GPU: a general CSR matrix (CsrMatrix)."""
+    xv = _as(x, np.float64)
+    if xv.size != a.n_cols:
+        raise Error(f"spmv_csr: x has length {xv.size}, expected {a.n_cols}")
     ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype))
     try:
         return ex.apply(xv)

@@ -86,6 +86,7 @@ class PlanInfo(C.Structure):
         ("m_cols", i32),
         ("rect_nnz", i64),
         ("gather_form", i32),
+        ("csr_cols", i32),
     ]
 
 
@@ -120,6 +121,7 @@ plan_create_partitioned = _sig(
     "csrc_gpu_plan_create_partitioned", C.c_int, PM, PS, P_i32, i32, C.POINTER(vp)
 )
 plan_create_band = _sig("csrc_gpu_plan_create_band", C.c_int, PM, PS, i32, i32, C.POINTER(vp))
+plan_create_csr = _sig("csrc_gpu_plan_create_csr", C.c_int, i32, i32, P_i32, P_i32, P_f64, PS, C.POINTER(vp))
 plan_create_rect = _sig("csrc_gpu_plan_create_rect", C.c_int, PM, PS, i32, P_i32, P_i32, P_f64,
                         C.POINTER(vp))
 plan_destroy = _sig("csrc_gpu_plan_destroy", None, vp)
@@ -176,7 +178,7 @@ built_free = _sig("csrc_built_free", None, vp)
 EXPORTED = [
     "csrc_gpu_last_error", "csrc_gpu_abi_version", "csrc_gpu_device_count",
     "csrc_gpu_plan_create", "csrc_gpu_plan_create_colored", "csrc_gpu_plan_create_partitioned",
-    "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
+    "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_create_csr", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
     "csrc_gpu_gather_interior", "csrc_gpu_spmv_device_rows",

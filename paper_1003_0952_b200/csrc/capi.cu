@@ -194,7 +194,9 @@ struct csrc_gpu_plan_s {
     DevBuf rt_ptr, rt_col, rt_val;
 
     size_t vsize() const { return dtype == CSRC_DTYPE_F32 ? 4 : 8; }
-    index_t x_len() const { return m_cols ? m_cols : n_global; }
+    bool is_csr = false;   // CSR plan (csrc_gpu_plan_create_csr)
+    index_t csr_cols = 0;  // its columns (x length)
+    index_t x_len() const { return m_cols ? m_cols : (is_csr ? csr_cols : n_global); }
     index_t vec_len() const { return row_end - lo; }
     index_t x_hi = 0;  // gather: end of the x range the plan reads (band plans: above row_end)
     // gather band plans: rows [gi0, gi1) (band-relative, 256-aligned inward) read
@@ -934,6 +936,10 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const HVec
 }
 
 template <class T>
+void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HVec<int32_t>& eidx,
+                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace);
+
+template <class T>
 void setup_gather(Plan& P, const MatView& a) {
     // rows [r0, r1) of the global matrix (the whole matrix unless a band plan);
     // entry columns are stored in band-row coordinates (c - r0, negative below
@@ -1042,6 +1048,24 @@ void setup_gather(Plan& P, const MatView& a) {
         P.gi1 = std::max(P.gi0, a1);
     }
     mark("interior split");
+    finish_gather<T>(P, n, band, eptr, eidx, ev, evt, a.value_symmetric, trace);
+}
+
+// Second half of a gather plan, shared by the CSRC plans (setup_gather) and
+// the CSR plans (setup_gather_csr): host pipeline chunks, row patterns, kernel
+// form (staged / sliced / rows), uploads.
+template <class T>
+void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HVec<int32_t>& eidx,
+                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace) {
+    const size_t ne = static_cast<size_t>(eptr[n]);
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "gather plan: %-22s %8.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t_last).count());
+        t_last = t;
+    };
     const double avg = n ? static_cast<double>(ne) / n : 0.0;
     P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? 2 : avg <= 128 ? 4 : 8);
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
@@ -1150,13 +1174,13 @@ void setup_gather(Plan& P, const MatView& a) {
     const bool sell_auto = has_pat && avg > 40.0;  // (not P.gather_pat: explicit columns keep the same form)
     mark("staged-kernel config");
     if ((sell_env == 1 || (sell_env < 0 && sell_auto)) && n > 0) {
-        setup_sell<T>(P, n, eptr, eidx, ev, evt, a.value_symmetric, pbase, pat_off);
+        setup_sell<T>(P, n, eptr, eidx, ev, evt, value_symmetric, pbase, pat_off);
         mark("sliced layout + upload");
         return;
     }
     upload(P.eptr, eptr.data(), eptr.size());
     upload_values<T>(P.eval, ev.data(), ev.size());
-    if (!a.value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
+    if (!value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
     mark("value uploads");
     if (!P.gather_buf) P.gather_pat = 0;  // the plain row kernel reads explicit indices
     if (P.gather_pat) {
@@ -1166,6 +1190,26 @@ void setup_gather(Plan& P, const MatView& a) {
         P.n_patterns = 0;
         upload(P.eidx, eidx.data(), eidx.size());
     }
+}
+
+// CSR plan (spmv_csr, kernels.hpp:7-22): the CSR rows are the entry stream
+// as they stand (diagonal included, no ad term, no transposed stream).
+template <class T>
+void setup_gather_csr(Plan& P, index_t n_rows, index_t n_cols, const int32_t* rp, const int32_t* ci,
+                      const double* va) {
+    const int64_t nnz = rp[n_rows];
+    std::vector<int32_t> eptr(rp, rp + n_rows + 1);
+    HVec<int32_t> eidx(static_cast<size_t>(nnz));
+    HVec<double> ev(static_cast<size_t>(nnz)), evt;
+    parallel_slices(nnz, [&](int, int64_t b, int64_t e) {
+        std::memcpy(eidx.data() + b, ci + b, static_cast<size_t>(e - b) * sizeof(int32_t));
+        std::memcpy(ev.data() + b, va + b, static_cast<size_t>(e - b) * sizeof(double));
+    });
+    P.x_hi = n_cols;
+    P.gi0 = P.gi1 = 0;
+    // rectangular CSR: no host pipeline (its x chunks follow the rows)
+    finish_gather<T>(P, n_rows, n_rows != n_cols, eptr, eidx, ev, evt, true,
+                     env_int("CSRC_GPU_PLAN_TRACE", 0) != 0);
 }
 
 template <class T, int L, int PF>
@@ -1634,6 +1678,7 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
 }
 
 void apply_device(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, int part = -1) {
+    if (tr && P.is_csr) throw Error("spmv_csr: CSR plans have no transpose product");
     if (P.nrows == 0) return;
     CUDA_OK(cudaSetDevice(P.device));
     if (P.dtype == CSRC_DTYPE_F64)
@@ -1741,8 +1786,8 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
 
 void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
     if (x_len != P.x_len())
-        throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +
-                    std::to_string(P.x_len()));
+        throw Error(std::string(P.is_csr ? "spmv_csr" : "ParallelSpmv") + ": x has length " + std::to_string(x_len) +
+                    ", expected " + std::to_string(P.x_len()));
     if (P.row_begin != 0 || P.row_end != P.n_global)
         throw Error("host products need a full-matrix plan (use the device entry points for bands)");
     if (P.n_global == 0) return;
@@ -1772,6 +1817,49 @@ void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
         CUDA_OK(cudaMemcpyAsync(yh, P.dyd.p, n * 8, cudaMemcpyDeviceToHost, st));
     }
     CUDA_OK(cudaStreamSynchronize(st));
+}
+
+Plan* create_csr_plan(int32_t n_rows, int32_t n_cols, const int32_t* rp, const int32_t* ci, const double* va,
+                      const csrc_gpu_strategy* s) {
+    if (!s) throw Error("null strategy");
+    if (s->kind != CSRC_KIND_SEQUENTIAL && s->kind != CSRC_KIND_GATHER)
+        throw Error("CSR plans run the gather kernel (strategy sequential or gather)");
+    if (s->dtype != CSRC_DTYPE_F64 && s->dtype != CSRC_DTYPE_F32)
+        throw Error("unknown dtype " + std::to_string(s->dtype));
+    if (n_rows < 0 || n_cols < 0) throw Error("spmv_csr: negative dimensions");
+    if (!rp || rp[0] != 0) throw Error("spmv_csr: row_ptr must start at 0");
+    for (index_t i = 0; i < n_rows; ++i)
+        if (rp[i + 1] < rp[i]) throw Error("spmv_csr: row_ptr not nondecreasing at row " + std::to_string(i));
+    const int64_t nnz = rp[n_rows];
+    if (nnz > 0 && (!ci || !va)) throw Error("spmv_csr: null column or value array");
+    for (int64_t q = 0; q < nnz; ++q)
+        if (ci[q] < 0 || ci[q] >= n_cols)
+            throw Error("spmv_csr: column " + std::to_string(ci[q]) + " outside [0, " + std::to_string(n_cols) + ")");
+    auto P = std::make_unique<Plan>();
+    P->device = s->device;
+    CUDA_OK(cudaSetDevice(P->device));
+    P->kind = CSRC_KIND_GATHER;
+    P->exec_kind = CSRC_KIND_GATHER;
+    P->dtype = s->dtype;
+    P->p_ref = s->p;
+    P->n_global = n_rows;
+    P->row_begin = 0;
+    P->row_end = n_rows;
+    P->lo = 0;
+    P->nrows = n_rows;
+    P->k = nnz;
+    P->value_symmetric = true;  // one value stream: no transpose product for CSR plans
+    P->is_csr = true;
+    P->csr_cols = n_cols;
+    P->launches = 1;
+    CUDA_OK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+    for (auto& e : P->ev) CUDA_OK(cudaEventCreate(&e));
+    if (n_rows == 0) return P.release();
+    if (P->dtype == CSRC_DTYPE_F64)
+        setup_gather_csr<double>(*P, n_rows, n_cols, rp, ci, va);
+    else
+        setup_gather_csr<float>(*P, n_rows, n_cols, rp, ci, va);
+    return P.release();
 }
 
 Plan* checked(csrc_gpu_plan_t p) {
@@ -1810,6 +1898,15 @@ int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strat
         o.color = color;
         o.n_colors = n_colors;
         *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_create_csr(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, const int32_t* col_idx,
+                             const double* values, const csrc_gpu_strategy* s, csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out) throw Error("null output");
+        *out = nullptr;
+        *out = create_csr_plan(n_rows, n_cols, row_ptr, col_idx, values, s);
     });
 }
 
@@ -1923,6 +2020,12 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
                                             : 0;
         }
         info->gather_form = P.exec_kind != CSRC_KIND_GATHER ? 0 : P.gather_sell ? 3 : P.gather_buf ? 2 : 1;
+        info->csr_cols = P.csr_cols;
+        if (P.is_csr) {  // CSR model: values + columns + row pointers + x + y
+            const int64_t vs = static_cast<int64_t>(P.vsize());
+            info->model_bytes = P.k * (vs + 4) + 4 * (static_cast<int64_t>(P.nrows) + 1) +
+                                vs * (static_cast<int64_t>(P.csr_cols) + P.nrows);
+        }
         info->m_cols = P.m_cols;
         info->rect_nnz = P.rect_nnz;
         if (P.m_cols) {
@@ -1946,6 +2049,7 @@ int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t 
     return guarded([&] {
         Plan& P = *checked(plan);
         if (P.m_cols) throw Error("spmv_csrc_transpose: rectangular plans have no transpose product");
+        if (P.is_csr) throw Error("spmv_csr: CSR plans have no transpose product");
         if (x_len != P.n_global)
             throw Error("spmv_csrc_transpose: x has length " + std::to_string(x_len) +
                         ", expected " + std::to_string(P.n_global));

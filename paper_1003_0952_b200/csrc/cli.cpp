@@ -509,6 +509,10 @@ struct Plan {
         else
             ck(csrc_gpu_plan_create(&m, &s, &h));
     }
+    Plan(const Csr& a, const csrc_gpu_strategy& s) {  // spmv_csr plan
+        ck(csrc_gpu_plan_create_csr(a.n_rows, a.n_cols, a.rp.data(), a.ci.data(), a.va.data(), &s, &h));
+    }
+    Plan(Plan&& o) noexcept : h(o.h) { o.h = nullptr; }
     ~Plan() { csrc_gpu_plan_destroy(h); }
     Plan(const Plan&) = delete;
     Plan& operator=(const Plan&) = delete;
@@ -697,7 +701,7 @@ int do_run(const Args& A) {
     const int accum = accum_of(A.accum);
     r.strategy = A.strategy;
     r.accum = kind == CSRC_KIND_LOCAL_BUFFERS ? accum_name(accum) : "-";
-    // csr format: the GPU's CSR product is the gather plan (the full matrix row by row)
+    // csr format: a CSR plan over the full matrix (spmv_csr, kernels.hpp:7-22)
     const bool csr = A.format == "csr";
     r.format = csr ? "csr" : (m.value_symmetric ? "csrc_sym" : "csrc");
     if (csr) kind = CSRC_KIND_GATHER;
@@ -709,16 +713,17 @@ int do_run(const Args& A) {
     const double base_med = base.total[median_index(base.total)];
 
     const bool sequential = kind == CSRC_KIND_SEQUENTIAL;
-    Plan exec(m, strategy(kind, accum, sequential ? 1 : A.threads, mode, dtype));
+    Plan exec = csr ? Plan(full, strategy(CSRC_KIND_GATHER, accum, 1, mode, dtype))
+                    : Plan(m, strategy(kind, accum, sequential ? 1 : A.threads, mode, dtype));
     if (kind == CSRC_KIND_COLORFUL) r.n_colors = exec.info().n_colors;
-    if (!sequential) {  // verify before timing (bench.hpp:221-228)
+    if (!sequential || csr) {  // verify before timing (bench.hpp:221-228)
         const double err = relative_error(exec.apply(x), y_ref);
         const double bound = dtype == CSRC_DTYPE_F32 ? 1e-5 : 1e-12;
         if (err > bound)
             throw Error("benchmark verification failed: relative error " + std::to_string(err) +
                         " vs sequential CSRC");
     }
-    const RunTimes rt = sequential ? base : time_plan(exec, x, A.reps, A.runs, A.host_vectors, dtype);
+    const RunTimes rt = sequential && !csr ? base : time_plan(exec, x, A.reps, A.runs, A.host_vectors, dtype);
     const size_t med = median_index(rt.total);
     r.median_total_seconds = rt.total[med];
     r.init_max = rt.init[med];
@@ -788,7 +793,10 @@ int do_verify(const Args& A) {
         return P.apply(x);
     };
     if (want("seq")) check("seq csrc p=1", run(CSRC_KIND_SEQUENTIAL, CSRC_ACCUM_EFFECTIVE, 1), true, "");
-    if (want("csr")) check("seq csr", run(CSRC_KIND_GATHER, CSRC_ACCUM_EFFECTIVE, 1), true, "");
+    if (want("csr")) {
+        Plan pc(full, strategy(CSRC_KIND_GATHER, CSRC_ACCUM_EFFECTIVE, 1, mode, CSRC_DTYPE_F64));
+        check("seq csr", pc.apply(x), true, "");
+    }
     for (const char* g : {"gather", "windowed", "atomic"})
         if (!A.only.empty() && A.only == g) check(std::string(g) + " p=1", run(kind_of(g), CSRC_ACCUM_EFFECTIVE, 1), true, "");
     for (int p : int_list(A.threads_list)) {

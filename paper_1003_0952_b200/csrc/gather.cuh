@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(256) k_gather_rows(const int32_t* __restrict__
         }
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
-        if (act && sub == 0) y[r] = s + __ldg(ad + r) * __ldg(x + r);
+        if (act && sub == 0) y[r] = ad ? s + __ldg(ad + r) * __ldg(x + r) : s;
     }
 }
 
@@ -233,8 +233,10 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
             eb = __ldg(A.eptr + row);
             ee = __ldg(A.eptr + row + 1);
             if (PAT) pb = __ldg(A.pbase + row) - eb;  // pattern slot of entry f = pb + f
-            d = __ldg(A.ad + row);
-            xr = __ldg(A.x + row);
+            if (A.ad) {  // CSR plans carry the diagonal in the entry stream (ad == nullptr)
+                d = __ldg(A.ad + row);
+                xr = __ldg(A.x + row);
+            }
         }
         const int32_t e_base = __ldg(A.eptr + base);  // the row block's first entry
         mbar_wait(&full[buf], NB == 2 ? ((it >> 1) & 1) : (it & 1));
@@ -270,7 +272,7 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         T s = acc0 + acc1;
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, L);
-        if (act && sub == 0) A.y[row] = s + d * xr;
+        if (act && sub == 0) A.y[row] = A.ad ? s + d * xr : s;
         __syncthreads();
         if (NB == 1 && threadIdx.x == 0 && base + stride < A.nrows) {
             issue(0, nx0, nx1, base + stride);  // single buffer: refill once every thread is done with it
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(256, SellMinBlocks<U>::value) k_gather_sell(co
         T sum = acc0 + acc1;
 #pragma unroll
         for (int off = L / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, L);
-        if (act && sub == 0) A.y[row] = sum + __ldg(A.ad + row) * __ldg(A.x + row);
+        if (act && sub == 0) A.y[row] = A.ad ? sum + __ldg(A.ad + row) * __ldg(A.x + row) : sum;
     }
 }
 

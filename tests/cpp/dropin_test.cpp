@@ -81,6 +81,12 @@ int main() {
         gpu::ParallelSpmv ex(ref_r, Strategy{StrategyKind::local_buffers, AccumMethod::interval, 4});
         worst = std::max(worst, max_rel(ex.apply(x), ref));
     }
+    // spmv_csr on the GPU against the reference's spmv_csr (kernels.hpp:7-22)
+    {
+        CsrMatrix full = build_csr(generate_random_sym(300, 0.04, 5));
+        Vector x = bench_source_vector(300);
+        worst = std::max(worst, max_rel(gpu::spmv_csr(full, x), spmv_csr(full, x)));
+    }
     // error behaviour: the reference's csrc::Error with its wording
     try {
         CsrcMatrix c = csr_to_csrc(build_csr(generate_band(10, 1)));

@@ -152,6 +152,10 @@ def test_run_reports_reference_fields(tmp_path):
         assert vals["strategy"] == strat
         if strat == "colorful":
             assert int(vals["n_colors"]) >= 2
+    r = cli("run", "--gen", "random_sym:n=3000,density=0.003,seed=4", "--format", "csr", "--reps", "20", "--runs", "1")
+    assert r.returncode == 0, r.stderr
+    vals = dict(zip(FIELDS, r.stdout.strip().splitlines()[1].split(",")))
+    assert vals["format"] == "csr" and float(vals["mflops_true"]) > 0
     r = cli("run", "--config", "c2", "--strategy", "gather", "--reps", "50", "--runs", "3", "--out", "csv",
             str(tmp_path / "c2.csv"))
     assert r.returncode == 0, r.stderr
