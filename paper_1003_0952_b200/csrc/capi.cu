@@ -697,50 +697,91 @@ int grid_for(int device, int64_t work, int per_block);
 // order); pbase[q] = start of row q's pattern in pat_off. Gives up (returns
 // false) past 65535 patterns or 1 M stored offsets: then the plan keeps
 // explicit column indices.
+// One dictionary of row offset patterns (local to a slice of rows, or global).
+struct PatternDict {
+    std::vector<int32_t> off, ptr{0};
+    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
+    // id of the pattern (o[0..len)), inserting it if new; -1 past the limits
+    int32_t find_or_add(const int32_t* o, int32_t len, uint64_t h) {
+        auto& cand = by_hash[h];
+        for (int32_t p : cand) {
+            const int32_t p0 = ptr[p];
+            if (ptr[p + 1] - p0 != len) continue;
+            if (std::equal(o, o + len, off.begin() + p0)) return p;
+        }
+        const int32_t id = static_cast<int32_t>(ptr.size()) - 1;
+        if (id >= 65535 || off.size() + len > (size_t(1) << 20)) return -1;
+        off.insert(off.end(), o, o + len);
+        ptr.push_back(static_cast<int32_t>(off.size()));
+        cand.push_back(id);
+        return id;
+    }
+};
+
+inline uint64_t pattern_hash(const int32_t* o, int32_t len) {
+    uint64_t h = 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(len);
+    for (int32_t j = 0; j < len; ++j) h = (h ^ static_cast<uint32_t>(o[j])) * 0x100000001B3ull;
+    return h;
+}
+
+// Dictionary of per-row column-offset patterns (offsets c - q in entry
+// order); pbase[q] = start of row q's pattern in pat_off. Gives up (returns
+// false) past 65535 patterns or 1 M stored offsets: then the plan keeps
+// explicit column indices. Row slices build local dictionaries in parallel;
+// merging them in slice order reproduces the serial first-occurrence order,
+// so the table and pbase are the same whatever the thread count.
 bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const HVec<int32_t>& eidx,
                        std::vector<int32_t>& pbase, std::vector<int32_t>& pat_off, int32_t* n_patterns) {
     pbase.assign(static_cast<size_t>(n), 0);
-    pat_off.clear();
-    std::vector<int32_t> pat_ptr(1, 0);
-    std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
-    int32_t prev = -1;  // consecutive rows usually share a pattern: try it first
-    for (index_t q = 0; q < n; ++q) {
-        const int32_t e0 = eptr[q], len = eptr[q + 1] - e0;
-        if (prev >= 0 && pat_ptr[prev + 1] - pat_ptr[prev] == len) {
-            const int32_t p0 = pat_ptr[prev];
-            bool same = true;
-            for (int32_t j = 0; j < len && same; ++j) same = pat_off[p0 + j] == eidx[e0 + j] - q;
-            if (same) {
-                pbase[q] = p0;
+    std::vector<int32_t> lid(static_cast<size_t>(n));
+    std::vector<PatternDict> local(64);
+    std::vector<char> failed(64, 0);
+    int slices = 0;
+    parallel_slices(n, [&](int t, int64_t b, int64_t e) {
+        PatternDict& D = local[t];
+        std::vector<int32_t> o;
+        int32_t prev = -1;  // consecutive rows usually share a pattern: try it first
+        for (index_t q = static_cast<index_t>(b); q < e; ++q) {
+            const int32_t e0 = eptr[q], len = eptr[q + 1] - e0;
+            o.resize(static_cast<size_t>(len));
+            for (int32_t j = 0; j < len; ++j) o[j] = eidx[e0 + j] - q;
+            if (prev >= 0 && D.ptr[prev + 1] - D.ptr[prev] == len &&
+                std::equal(o.begin(), o.end(), D.off.begin() + D.ptr[prev])) {
+                lid[q] = prev;
                 continue;
             }
-        }
-        uint64_t h = 0x9E3779B97F4A7C15ull ^ static_cast<uint64_t>(len);
-        for (int32_t j = 0; j < len; ++j)
-            h = (h ^ static_cast<uint32_t>(eidx[e0 + j] - q)) * 0x100000001B3ull;
-        auto& cand = by_hash[h];
-        int32_t found = -1;
-        for (int32_t p : cand) {
-            const int32_t p0 = pat_ptr[p];
-            if (pat_ptr[p + 1] - p0 != len) continue;
-            bool same = true;
-            for (int32_t j = 0; j < len && same; ++j) same = pat_off[p0 + j] == eidx[e0 + j] - q;
-            if (same) {
-                found = p;
-                break;
+            const int32_t id = D.find_or_add(o.data(), len, pattern_hash(o.data(), len));
+            if (id < 0) {
+                failed[t] = 1;
+                return;
             }
+            lid[q] = prev = id;
         }
-        if (found < 0) {
-            found = static_cast<int32_t>(pat_ptr.size()) - 1;
-            if (found >= 65535 || pat_off.size() + len > (size_t(1) << 20)) return false;
-            for (int32_t j = 0; j < len; ++j) pat_off.push_back(eidx[e0 + j] - q);
-            pat_ptr.push_back(static_cast<int32_t>(pat_off.size()));
-            cand.push_back(found);
-        }
-        pbase[q] = pat_ptr[found];
-        prev = found;
+    });
+    for (int t = 0; t < 64; ++t) {
+        if (failed[t]) return false;
+        if (local[t].ptr.size() > 1 || t == 0) slices = t + 1;
     }
-    *n_patterns = static_cast<int32_t>(pat_ptr.size()) - 1;
+    // merge in slice order: global ids by first occurrence, as a serial pass
+    PatternDict G;
+    std::vector<std::vector<int32_t>> to_global(static_cast<size_t>(slices));
+    for (int t = 0; t < slices; ++t) {
+        const PatternDict& D = local[t];
+        const int np = static_cast<int>(D.ptr.size()) - 1;
+        to_global[t].resize(static_cast<size_t>(np));
+        for (int p = 0; p < np; ++p) {
+            const int32_t* o = D.off.data() + D.ptr[p];
+            const int32_t len = D.ptr[p + 1] - D.ptr[p];
+            const int32_t g = G.find_or_add(o, len, pattern_hash(o, len));
+            if (g < 0) return false;
+            to_global[t][p] = G.ptr[g];  // pattern start in the global table
+        }
+    }
+    parallel_slices(n, [&](int t, int64_t b, int64_t e) {
+        for (index_t q = static_cast<index_t>(b); q < e; ++q) pbase[q] = to_global[t][lid[q]];
+    });
+    *n_patterns = static_cast<int32_t>(G.ptr.size()) - 1;
+    pat_off = std::move(G.off);
     if (pat_off.empty()) pat_off.push_back(0);  // keep the device table non-empty
     return true;
 }
