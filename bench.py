@@ -272,8 +272,13 @@ def main():
             otot, oker = ox.time_products(xd, yd, min(args.steps, 50), flush)
             ox.close()
             oms = float(np.mean(otot))
+            okms = float(np.mean(oker))
+            peak_o, _ = load_peaks()
             others[name] = dict(ms_per_step=oms, gflops=flops / (oms / 1e3) / 1e9,
-                                effective_gbs=mb / (oms / 1e3) / 1e9, kernel_ms=float(np.mean(oker)))
+                                effective_gbs=mb / (oms / 1e3) / 1e9, kernel_ms=okms,
+                                roofline_achieved_gbs=mb / (okms / 1e3) / 1e9,
+                                roofline_frac=mb / (okms / 1e3) / 1e9 / peak_o,
+                                reads_csrc_as_stored=name in ("windowed", "atomic"))
         # end to end through the public host API: pinned x -> device, product, y -> pinned host
         xh = torch.from_numpy(x).pin_memory()
         yh = torch.empty_like(xh).pin_memory()
