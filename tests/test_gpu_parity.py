@@ -248,6 +248,29 @@ def test_non_finite_x_and_ragged_sizes(env, monkeypatch):
             assert rel_l2(y[fin], ref[fin]) <= TOL64
 
 
+@pytest.mark.parametrize("env", [{}, {"CSRC_GPU_GSELL": "1"}, {"CSRC_GPU_GNT": "256"}, {"CSRC_GPU_WIN_RINGS": "1"}])
+def test_no_writes_outside_y(env, monkeypatch):
+    """Out-of-bounds write check (compute-sanitizer is not available on the
+    pool): y lives inside a larger buffer whose guard regions hold a sentinel;
+    every kernel kind must leave them untouched, for sizes that are not
+    multiples of a slice, row block or tile."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    guard = 4096
+    for key in ("g1_", "g2_", "g4_"):
+        a = MESH.matrix(key)
+        x = torch.from_numpy(MESH[key + "x"]).cuda()
+        for name, s in STRATEGIES:
+            ex = P.GpuSpmv(a, s)
+            buf = torch.full((a.n + 2 * guard,), 12345.0, dtype=torch.float64, device="cuda")
+            ex.apply_device(x, buf[guard:guard + a.n])
+            torch.cuda.synchronize()
+            assert bool((buf[:guard] == 12345.0).all()) and bool((buf[guard + a.n:] == 12345.0).all()), (key, name)
+            assert rel_l2(buf[guard:guard + a.n].cpu().numpy(), MESH[key + "y"]) <= TOL64, (key, name)
+            ex.close()
+
+
 def test_device_and_graph_entry_points():
     import torch
     a, x, _ = P.config_matrix("c1")
