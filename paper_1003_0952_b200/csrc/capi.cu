@@ -16,9 +16,13 @@
 #include <thread>
 #include <vector>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "hostlink.cuh"
 #include "internal.hpp"
 #include "kernels.cuh"
+#include "plan_device.cuh"
 
 using namespace csrcgpu;
 
@@ -73,6 +77,19 @@ void upload(DevBuf& d, const U* h, size_t count) {
     }
     cudaStreamDestroy(st);
 }
+
+void adopt(DevBuf& dst, DevBuf& src) {  // move a device allocation between buffers
+    if (dst.p) cudaFree(dst.p);
+    dst.p = src.p;
+    dst.bytes = src.bytes;
+    src.p = nullptr;
+    src.bytes = 0;
+}
+
+// per-row gather entries built on the device (plan_device.cuh)
+struct DevEntries {
+    DevBuf eidx, ev, evt;  // fp64 values; evt empty for value-symmetric matrices
+};
 
 int pow2_at_least(int64_t v) {
     int64_t p = 1;
@@ -978,7 +995,89 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const HVec
 
 template <class T>
 void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HVec<int32_t>& eidx,
-                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace);
+                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace,
+                   DevEntries* dv = nullptr);
+
+// Whole-matrix gather entries on the device: pairs stably radix-sorted by
+// column give each target row its upper pairs in ascending source row, the
+// serial host builder's order, so both builders produce the same plan.
+// Returns eptr and eidx on the host (patterns, pipeline chunks); the values
+// stay on the device.
+void build_entries_device(Plan& P, const MatView& a, std::vector<int32_t>& eptr, HVec<int32_t>& eidx,
+                          DevEntries& D) {
+    const index_t n = a.n;
+    const int64_t k = a.k, ne = 2 * k;
+    cudaStream_t st = P.stream;
+    DevBuf ia, ja, al, au, erow, up, cnt, ep, key, val, key2, val2, ust;
+    upload(ia, a.ia, static_cast<size_t>(n) + 1);
+    upload(ja, a.ja, static_cast<size_t>(k));
+    upload(al, a.al, static_cast<size_t>(k));
+    if (!a.value_symmetric) upload(au, a.au, static_cast<size_t>(k));
+    erow.alloc(static_cast<size_t>(k) * 4);
+    up.alloc((static_cast<size_t>(n) + 1) * 4);
+    cnt.alloc((static_cast<size_t>(n) + 1) * 4);
+    ep.alloc((static_cast<size_t>(n) + 1) * 4);
+    const unsigned gb = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(1, (k + 255) / 256), 1 << 20));
+    const unsigned gn = static_cast<unsigned>(std::min<int64_t>(std::max<int64_t>(1, (n + 255) / 256), 1 << 20));
+    CUDA_OK(cudaMemsetAsync(up.p, 0, (static_cast<size_t>(n) + 1) * 4, st));
+    CUDA_OK(cudaMemsetAsync(cnt.p, 0, (static_cast<size_t>(n) + 1) * 4, st));
+    dev::k_pair_rows<<<gn, 256, 0, st>>>(n, ia.as<int32_t>(), erow.as<int32_t>());
+    dev::k_upper_counts<<<gb, 256, 0, st>>>(k, ja.as<int32_t>(), up.as<int32_t>());
+    dev::k_row_counts<<<gn, 256, 0, st>>>(n, ia.as<int32_t>(), up.as<int32_t>(), cnt.as<int32_t>());
+    CUDA_OK(cudaGetLastError());
+    size_t tmp_bytes = 0;
+    CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt.as<int32_t>(), ep.as<int32_t>(), n + 1, st));
+    {
+        DevBuf tmp;
+        tmp.alloc(tmp_bytes);
+        CUDA_OK(cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, cnt.as<int32_t>(), ep.as<int32_t>(), n + 1, st));
+        CUDA_OK(cudaStreamSynchronize(st));
+    }
+    D.eidx.alloc(static_cast<size_t>(ne) * 4);
+    D.ev.alloc(static_cast<size_t>(ne) * 8);
+    if (!a.value_symmetric) D.evt.alloc(static_cast<size_t>(ne) * 8);
+    const double* aup = a.value_symmetric ? nullptr : au.as<double>();
+    dev::k_place_lower<<<gb, 256, 0, st>>>(k, erow.as<int32_t>(), ia.as<int32_t>(), ja.as<int32_t>(),
+                                           al.as<double>(), aup, ep.as<int32_t>(), D.eidx.as<int32_t>(),
+                                           D.ev.as<double>(), D.evt.as<double>());
+    CUDA_OK(cudaGetLastError());
+    // stable LSD radix sort of (column, pair) -> pairs grouped by column, rows ascending
+    key.alloc(static_cast<size_t>(k) * 4);
+    val.alloc(static_cast<size_t>(k) * 4);
+    key2.alloc(static_cast<size_t>(k) * 4);
+    val2.alloc(static_cast<size_t>(k) * 4);
+    CUDA_OK(cudaMemcpyAsync(key.p, ja.p, static_cast<size_t>(k) * 4, cudaMemcpyDeviceToDevice, st));
+    dev::k_iota<<<gb, 256, 0, st>>>(k, val.as<int32_t>());  // pair ids 0..k-1
+    CUDA_OK(cudaGetLastError());
+    int bits = 1;
+    while ((int64_t{1} << bits) < n) ++bits;
+    cub::DoubleBuffer<int32_t> kb(key.as<int32_t>(), key2.as<int32_t>()), vb(val.as<int32_t>(), val2.as<int32_t>());
+    tmp_bytes = 0;
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, kb, vb, static_cast<int>(k), 0, bits, st));
+    {
+        DevBuf tmp;
+        tmp.alloc(tmp_bytes);
+        CUDA_OK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, kb, vb, static_cast<int>(k), 0, bits, st));
+        ust.alloc((static_cast<size_t>(n) + 1) * 4);
+        size_t tb2 = 0;
+        CUDA_OK(cub::DeviceScan::ExclusiveSum(nullptr, tb2, up.as<int32_t>(), ust.as<int32_t>(), n + 1, st));
+        DevBuf tmp2;
+        tmp2.alloc(tb2);
+        CUDA_OK(cub::DeviceScan::ExclusiveSum(tmp2.p, tb2, up.as<int32_t>(), ust.as<int32_t>(), n + 1, st));
+        dev::k_place_upper<<<gb, 256, 0, st>>>(k, kb.Current(), vb.Current(), ust.as<int32_t>(), ia.as<int32_t>(),
+                                               erow.as<int32_t>(), al.as<double>(), aup, ep.as<int32_t>(),
+                                               D.eidx.as<int32_t>(), D.ev.as<double>(), D.evt.as<double>());
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaStreamSynchronize(st));
+    }
+    eptr.resize(static_cast<size_t>(n) + 1);
+    CUDA_OK(cudaMemcpy(eptr.data(), ep.p, (static_cast<size_t>(n) + 1) * 4, cudaMemcpyDeviceToHost));
+    eidx.resize(static_cast<size_t>(ne));
+    {
+        HostLink hl(st);
+        hl.d2h(eidx.data(), D.eidx.p, static_cast<size_t>(ne) * 4);
+    }
+}
 
 template <class T>
 void setup_gather(Plan& P, const MatView& a) {
@@ -994,6 +1093,26 @@ void setup_gather(Plan& P, const MatView& a) {
         throw Error("gather plan: more than 2^31 off-diagonal entries (use the windowed kernel)");
     // CSRC_GPU_PLAN_TRACE=1: phase times of the plan build on stderr (diagnostics)
     const bool trace = env_int("CSRC_GPU_PLAN_TRACE", 0) != 0;
+    if (!band && a.k >= (int64_t{1} << 20) && env_int("CSRC_GPU_PLAN_DEVICE", 0) != 0) {
+        // opt-in (CSRC_GPU_PLAN_DEVICE=1): the transposition on the device. The same
+        // plan bit for bit, but not faster: moving the 4.8 GB of CSRC arrays up and
+        // the 1.7 GB of entry columns down costs what the host transposition does
+        // (C5 1.29 s vs 1.15 s; profiles/r01_plan_build_trace_device.txt)
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<int32_t> eptr;
+        HVec<int32_t> eidx;
+        HVec<double> ev, evt;
+        DevEntries D;
+        build_entries_device(P, a, eptr, eidx, D);
+        P.x_hi = r1;
+        P.gi0 = 0;
+        P.gi1 = n;  // whole matrix: every column is one of the plan's rows
+        if (trace)
+            std::fprintf(stderr, "gather plan: %-22s %8.1f ms\n", "device entries",
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        finish_gather<T>(P, n, band, eptr, eidx, ev, evt, a.value_symmetric, trace, &D);
+        return;
+    }
     auto t_last = std::chrono::steady_clock::now();
     auto mark = [&](const char* what) {
         if (!trace) return;
@@ -1097,7 +1216,7 @@ void setup_gather(Plan& P, const MatView& a) {
 // form (staged / sliced / rows), uploads.
 template <class T>
 void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HVec<int32_t>& eidx,
-                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace) {
+                   HVec<double>& ev, HVec<double>& evt, bool value_symmetric, bool trace, DevEntries* dv) {
     const size_t ne = static_cast<size_t>(eptr[n]);
     auto t_last = std::chrono::steady_clock::now();
     auto mark = [&](const char* what) {
@@ -1215,13 +1334,39 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
     const bool sell_auto = has_pat && avg > 40.0;  // (not P.gather_pat: explicit columns keep the same form)
     mark("staged-kernel config");
     if ((sell_env == 1 || (sell_env < 0 && sell_auto)) && n > 0) {
+        if (dv) {  // the sliced layout is built on the host: fetch the device-built values
+            HostLink hl(P.stream);
+            ev.resize(ne);
+            hl.d2h(ev.data(), dv->ev.p, ne * 8);
+            if (!value_symmetric) {
+                evt.resize(ne);
+                hl.d2h(evt.data(), dv->evt.p, ne * 8);
+            }
+        }
         setup_sell<T>(P, n, eptr, eidx, ev, evt, value_symmetric, pbase, pat_off);
         mark("sliced layout + upload");
         return;
     }
     upload(P.eptr, eptr.data(), eptr.size());
-    upload_values<T>(P.eval, ev.data(), ev.size());
-    if (!value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
+    if (dv) {  // values already on the device (build_entries_device)
+        auto take = [&](DevBuf& dst, DevBuf& src) {
+            if (std::is_same<T, double>::value) {
+                adopt(dst, src);
+            } else {
+                dst.alloc(ne * sizeof(T));
+                dev::k_convert<double, float><<<grid_for(P.device, static_cast<int64_t>(ne), 256), 256, 0,
+                                                P.stream>>>(src.as<double>(), dst.as<float>(),
+                                                            static_cast<int64_t>(ne));
+                CUDA_OK(cudaGetLastError());
+                CUDA_OK(cudaStreamSynchronize(P.stream));
+            }
+        };
+        take(P.eval, dv->ev);
+        if (!value_symmetric) take(P.eval_t, dv->evt);
+    } else {
+        upload_values<T>(P.eval, ev.data(), ev.size());
+        if (!value_symmetric) upload_values<T>(P.eval_t, evt.data(), evt.size());
+    }
     mark("value uploads");
     if (!P.gather_buf) P.gather_pat = 0;  // the plain row kernel reads explicit indices
     if (P.gather_pat) {
@@ -1229,7 +1374,10 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
         upload(P.pat_off, pat_off.data(), pat_off.size());
     } else {
         P.n_patterns = 0;
-        upload(P.eidx, eidx.data(), eidx.size());
+        if (dv)
+            adopt(P.eidx, dv->eidx);
+        else
+            upload(P.eidx, eidx.data(), eidx.size());
     }
 }
 

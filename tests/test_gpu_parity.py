@@ -271,6 +271,33 @@ def test_no_writes_outside_y(env, monkeypatch):
             ex.close()
 
 
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c4"])
+def test_device_plan_build_equals_host_build(cfg, monkeypatch):
+    """The opt-in device builder of whole-matrix gather plans
+    (CSRC_GPU_PLAN_DEVICE=1: stable radix sort of the pairs by column) must
+    give the host builder's plan: identical products, bit for bit, normal and
+    transposed, fp64 and fp32."""
+    import torch
+    a, x, _ = P.config_matrix(cfg)
+    xd = torch.from_numpy(x).cuda()
+    for dt, tdt in ((P.DType.f64, torch.float64), (P.DType.f32, torch.float32)):
+        out = []
+        for dev_build in ("1", "0"):
+            monkeypatch.setenv("CSRC_GPU_PLAN_DEVICE", dev_build)
+            ex = P.GpuSpmv(a, P.Strategy(K.gather, dtype=dt))
+            xin = xd.to(tdt)
+            y = torch.empty_like(xin)
+            yt = torch.empty_like(xin)
+            ex.apply_device(xin, y)
+            ex.apply_device(xin, yt, transpose=True)
+            torch.cuda.synchronize()
+            out.append((y.cpu().numpy(), yt.cpu().numpy(), ex.info().row_patterns, ex.info().gather_form))
+            ex.close()
+        assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1]), (cfg, dt)
+        assert out[0][2:] == out[1][2:]
+    assert rel_l2(out[0][0], O.spmv_csrc(round32(a), x.astype(np.float32).astype(np.float64))) <= TOL32
+
+
 def test_device_and_graph_entry_points():
     import torch
     a, x, _ = P.config_matrix("c1")
