@@ -177,6 +177,12 @@ struct csrc_gpu_plan_s {
     std::vector<int32_t> hneed;
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaStream_t s_h2d2 = nullptr, s_d2h2 = nullptr;  // optional second copy streams
+    // pageable user vectors (std::vector in the reference's API) are staged
+    // through these pinned buffers by a persistent copy pool, chunk by chunk
+    std::unique_ptr<CopyPool> cpool;
+    double* hx_pin = nullptr;
+    double* hy_pin = nullptr;
+    std::vector<cudaEvent_t> ev_d;  // D2H of y chunk c complete
     cudaEvent_t ev_in = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
 
@@ -233,6 +239,10 @@ struct csrc_gpu_plan_s {
         if (s_d2h) cudaStreamDestroy(s_d2h);
         if (s_h2d2) cudaStreamDestroy(s_h2d2);
         if (s_d2h2) cudaStreamDestroy(s_d2h2);
+        for (auto& e : ev_d)
+            if (e) cudaEventDestroy(e);
+        if (hx_pin) cudaFreeHost(hx_pin);
+        if (hy_pin) cudaFreeHost(hy_pin);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -1882,6 +1892,29 @@ void apply_device(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, i
 // s_d2h while later chunks compute. H2D and D2H use the two copy directions
 // of the link concurrently. Same kernels and summation order as the device
 // entry point, so results are bit-identical to it.
+// Pinned staging for pageable host vectors (lazily, once per plan).
+void ensure_staging(Plan& P, bool x_stage, bool y_stage) {
+    if ((x_stage || y_stage) && !P.cpool) {
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        P.cpool = std::make_unique<CopyPool>(std::min(hw, 16));
+    }
+    if (x_stage && !P.hx_pin)
+        CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&P.hx_pin), static_cast<size_t>(P.x_len()) * 8,
+                              cudaHostAllocDefault));
+    if (y_stage && !P.hy_pin)
+        CUDA_OK(cudaHostAlloc(reinterpret_cast<void**>(&P.hy_pin), static_cast<size_t>(P.n_global) * 8,
+                              cudaHostAllocDefault));
+}
+
+// Host product with the copies overlapped (gather plans): x goes up in row
+// chunks on s_h2d; chunk c's rows run on the compute stream once the last x
+// chunk they read (hneed[c], plan time) has landed; its y rows go down on
+// s_d2h while later chunks compute. H2D and D2H use the two copy directions
+// of the link concurrently. Pageable x / y (the reference API's std::vector)
+// are staged through pinned buffers by the copy pool inside the same chunk
+// loop: chunk c+1 of x is copied while chunk c is on the link, and finished y
+// chunks are copied out while later x chunks still stage. Same kernels and
+// summation order as the device entry point, so results are bit-identical.
 void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
     const int nc = static_cast<int>(P.hchunk.size()) - 1;
     if (!P.s_h2d) {
@@ -1892,11 +1925,17 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         CUDA_OK(cudaEventCreateWithFlags(&P.ev_in, cudaEventDisableTiming));
         P.ev_x.assign(nc, nullptr);
         P.ev_y.assign(nc, nullptr);
+        P.ev_d.assign(nc, nullptr);
         for (int c = 0; c < nc; ++c) {
             CUDA_OK(cudaEventCreateWithFlags(&P.ev_x[c], cudaEventDisableTiming));
             CUDA_OK(cudaEventCreateWithFlags(&P.ev_y[c], cudaEventDisableTiming));
+            CUDA_OK(cudaEventCreateWithFlags(&P.ev_d[c], cudaEventDisableTiming));
         }
     }
+    const bool xs = !host_pinned(xh), ys = !host_pinned(yh);
+    ensure_staging(P, xs, ys);
+    const double* xsrc = xs ? P.hx_pin : xh;
+    double* ydst = ys ? P.hy_pin : yh;
     const bool f32 = P.dtype == CSRC_DTYPE_F32;
     if (f32) {
         const size_t n = static_cast<size_t>(P.n_global);
@@ -1921,15 +1960,8 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
     CUDA_OK(cudaEventRecord(P.ev_in, st));
     CUDA_OK(cudaStreamWaitEvent(P.s_h2d, P.ev_in, 0));  // after earlier work on the plan stream
     if (h2d2) CUDA_OK(cudaStreamWaitEvent(P.s_h2d2, P.ev_in, 0));
-    for (int c = 0; c < nc; ++c) {
-        const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
-        cudaStream_t sc = h2d2 && (c & 1) ? P.s_h2d2 : P.s_h2d;
-        CUDA_OK(cudaMemcpyAsync(xd64 + r0, xh + r0, len * 8, cudaMemcpyHostToDevice, sc));
-        CUDA_OK(cudaEventRecord(P.ev_x[c], sc));
-        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + c], sc));
-    }
     int have = -1;  // x chunks the compute stream already waited for (and converted)
-    for (int c = 0; c < nc; ++c) {
+    auto compute_chunk = [&](int c) {
         for (; have < P.hneed[c]; ++have) {
             CUDA_OK(cudaStreamWaitEvent(st, P.ev_x[have + 1], 0));
             if (f32) {
@@ -1951,10 +1983,34 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + nc + c], st));
         cudaStream_t sd = d2h2 && (c & 1) ? P.s_d2h2 : P.s_d2h;
         CUDA_OK(cudaStreamWaitEvent(sd, P.ev_y[c], 0));
-        CUDA_OK(cudaMemcpyAsync(yh + r0, yd64 + r0, static_cast<size_t>(r1 - r0) * 8,
+        CUDA_OK(cudaMemcpyAsync(ydst + r0, yd64 + r0, static_cast<size_t>(r1 - r0) * 8,
                                 cudaMemcpyDeviceToHost, sd));
+        CUDA_OK(cudaEventRecord(P.ev_d[c], sd));
         if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + 2 * nc + c], sd));
+    };
+    int next_c = 0, next_out = 0;  // chunks enqueued for compute / copied out to a pageable y
+    auto copy_out = [&](bool block) {
+        for (; next_out < next_c; ++next_out) {
+            if (block)
+                CUDA_OK(cudaEventSynchronize(P.ev_d[next_out]));
+            else if (cudaEventQuery(P.ev_d[next_out]) != cudaSuccess)
+                break;
+            const size_t r0 = P.hchunk[next_out], len = P.hchunk[next_out + 1] - P.hchunk[next_out];
+            P.cpool->copy(yh + r0, P.hy_pin + r0, len * 8);
+        }
+    };
+    for (int c = 0; c < nc; ++c) {
+        const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
+        if (xs) P.cpool->copy(P.hx_pin + r0, xh + r0, len * 8);
+        cudaStream_t sc = h2d2 && (c & 1) ? P.s_h2d2 : P.s_h2d;
+        CUDA_OK(cudaMemcpyAsync(xd64 + r0, xsrc + r0, len * 8, cudaMemcpyHostToDevice, sc));
+        CUDA_OK(cudaEventRecord(P.ev_x[c], sc));
+        if (trace) CUDA_OK(cudaEventRecord(tr_ev[1 + c], sc));
+        for (; next_c < nc && P.hneed[next_c] <= c; ++next_c) compute_chunk(next_c);
+        if (ys) copy_out(false);
     }
+    for (; next_c < nc; ++next_c) compute_chunk(next_c);
+    if (ys) copy_out(true);
     CUDA_OK(cudaStreamSynchronize(P.s_d2h));
     if (d2h2) CUDA_OK(cudaStreamSynchronize(P.s_d2h2));
     if (h2d2) CUDA_OK(cudaStreamSynchronize(P.s_h2d2));
@@ -1990,6 +2046,15 @@ void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
         apply_host_pipelined(P, xh, yh, tr);
         return;
     }
+    // pageable x / y: whole-vector staging through the plan's pinned buffers
+    const bool xs = !host_pinned(xh), ys = !host_pinned(yh);
+    ensure_staging(P, xs, ys);
+    double* const y_user = yh;
+    if (xs) {
+        P.cpool->copy(P.hx_pin, xh, nx * 8);
+        xh = P.hx_pin;
+    }
+    if (ys) yh = P.hy_pin;
     if (P.dtype == CSRC_DTYPE_F64) {
         CUDA_OK(cudaMemcpyAsync(P.dx.p, xh, nx * 8, cudaMemcpyHostToDevice, st));
         apply_device(P, P.dx.p, P.dy.p, st, tr);
@@ -2006,6 +2071,7 @@ void apply_host(Plan& P, const double* xh, int64_t x_len, double* yh, bool tr) {
         CUDA_OK(cudaMemcpyAsync(yh, P.dyd.p, n * 8, cudaMemcpyDeviceToHost, st));
     }
     CUDA_OK(cudaStreamSynchronize(st));
+    if (ys) P.cpool->copy(y_user, P.hy_pin, n * 8);
 }
 
 Plan* create_csr_plan(int32_t n_rows, int32_t n_cols, const int32_t* rp, const int32_t* ci, const double* va,

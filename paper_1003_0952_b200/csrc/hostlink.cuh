@@ -139,3 +139,90 @@ private:
 
 
 }  // namespace csrcgpu
+
+#include <condition_variable>
+#include <mutex>
+
+namespace csrcgpu {
+
+// Persistent fork-join memcpy pool: the host API stages pageable user vectors
+// (the reference's std::vector) through pinned buffers chunk by chunk, so the
+// copies must be parallel and cheap to start (no thread spawn per chunk).
+class CopyPool {
+public:
+    explicit CopyPool(int threads) : T_(std::max(1, threads)) {
+        for (int id = 1; id < T_; ++id) th_.emplace_back([this, id] { worker(id); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    CopyPool(const CopyPool&) = delete;
+    CopyPool& operator=(const CopyPool&) = delete;
+
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (bytes < (size_t(1) << 20) || T_ == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        {
+            std::lock_guard<std::mutex> g(m_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            pending_ = T_ - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> g(m_);
+        done_cv_.wait(g, [this] { return pending_ == 0; });
+    }
+
+private:
+    void part(int id) const {
+        const size_t per = (bytes_ / T_ + 63) & ~size_t(63);
+        const size_t o = per * static_cast<size_t>(id);
+        if (o < bytes_) std::memcpy(dst_ + o, src_ + o, std::min(per, bytes_ - o));
+    }
+    void worker(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(m_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            part(id);
+            std::lock_guard<std::mutex> g(m_);
+            if (--pending_ == 0) done_cv_.notify_one();
+        }
+    }
+    int T_;
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    int pending_ = 0;
+    bool stop_ = false;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+inline bool host_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace csrcgpu
