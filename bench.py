@@ -224,11 +224,21 @@ def main():
     import torch
     import paper_1003_0952_b200 as P
 
+    # CSRC_BENCH_SHARE_GPU=1 (functional check of the N>1 code path on a one-GPU box, gather bands only:
+    # their kernels never wait on each other): ranks share the visible GPUs and the timing collectives
+    # run over gloo. Its numbers are not measurements.
+    share = os.environ.get("CSRC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
+    coll_dev = "cpu" if share else "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dtype = P.DType.f32 if args.dtype == "f32" else P.DType.f64
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     a, x, _ = P.config_matrix(args.config)
@@ -314,7 +324,7 @@ def main():
         dist.barrier()
         clocks = cs.summary()
         ms = e0.elapsed_time(e1) / args.steps
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
         kms = ms
@@ -331,7 +341,7 @@ def main():
             yh.copy_(yd[p.row_begin - p.y_lo:].to(torch.float64), non_blocking=True)
             torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.steps
-        te = torch.tensor([e2e_s], device="cuda")
+        te = torch.tensor([e2e_s], device=coll_dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
         ds.close()

@@ -496,23 +496,41 @@ class GpuSpmv:
             return t
         return int(t.data_ptr())
 
+    @staticmethod
+    def _stream(stream, t=None):
+        """The cudaStream_t a device call enqueues on. An int is a raw handle
+        (0 = the plan's own stream, as in the C ABI). None with torch tensors
+        = torch's current stream on the tensor's device, like any torch op;
+        None with raw pointers = the plan's stream. Torch's default stream is
+        the legacy NULL stream: it is passed as cudaStreamLegacy (handle 1),
+        because a NULL handle means the plan's (non-blocking) stream."""
+        if isinstance(stream, int):
+            return stream or None
+        if stream is None:
+            if t is None or isinstance(t, int):
+                return None
+            import torch
+            stream = torch.cuda.current_stream(t.device)
+        return int(stream.cuda_stream) or 1
+
     def apply_device(self, x, y, stream=None, transpose: bool = False) -> None:
-        st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
-        _check(L.spmv_device(self._h, self._ptr(x), self._ptr(y), st or None,
+        """y = A x on device tensors (or raw pointers), enqueued on `stream`
+        (default: torch's current stream, see _stream)."""
+        _check(L.spmv_device(self._h, self._ptr(x), self._ptr(y), self._stream(stream, x),
                              1 if transpose else 0))
 
     def apply_device_graph(self, x, y, stream=None) -> None:
+        """apply_device replayed from a CUDA graph. stream None = the plan's
+        own stream (a graph cannot be captured on the legacy NULL stream)."""
         st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
         _check(L.spmv_device_graph(self._h, self._ptr(x), self._ptr(y), st or None))
 
     def apply_device_part(self, x, y, part: int, stream=None) -> None:
-        st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
-        _check(L.spmv_device_part(self._h, self._ptr(x), self._ptr(y), st or None, part))
+        _check(L.spmv_device_part(self._h, self._ptr(x), self._ptr(y), self._stream(stream, x), part))
 
     def halo_accumulate(self, y, dst_off: int, recv, length: int, stream=None) -> None:
-        st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
         _check(L.halo_accumulate(self._h, self._ptr(y), dst_off, self._ptr(recv), length,
-                                 st or None))
+                                 self._stream(stream, y)))
 
     def gather_interior(self) -> Tuple[int, int]:
         """Rows (plan-relative) that read x only on the plan's own rows."""
@@ -523,8 +541,8 @@ class GpuSpmv:
     def apply_device_rows(self, x, y, rows_begin: int, rows_end: int, stream=None,
                           transpose: bool = False) -> None:
         """Gather plans: the product on rows [rows_begin, rows_end) only."""
-        st = stream if isinstance(stream, int) else (stream.cuda_stream if stream else 0)
-        _check(L.spmv_device_rows(self._h, self._ptr(x), self._ptr(y), st or None, 1 if transpose else 0,
+        _check(L.spmv_device_rows(self._h, self._ptr(x), self._ptr(y), self._stream(stream, x),
+                                  1 if transpose else 0,
                                   int(rows_begin), int(rows_end)))
 
     def band_split(self) -> int:

@@ -1960,6 +1960,16 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
     CUDA_OK(cudaEventRecord(P.ev_in, st));
     CUDA_OK(cudaStreamWaitEvent(P.s_h2d, P.ev_in, 0));  // after earlier work on the plan stream
     if (h2d2) CUDA_OK(cudaStreamWaitEvent(P.s_h2d2, P.ev_in, 0));
+    // CSRC_GPU_HOST_GRID_DIV=d: chunk products on 1/d of the usual grid (diagnostics: leaves HBM
+    // headroom for the copy engines' writes while the link is the bottleneck)
+    const int grid_div = std::max(1, env_int("CSRC_GPU_HOST_GRID_DIV", 1));
+    struct GridRestore {
+        Plan& p;
+        int g, s;
+        ~GridRestore() { p.gather_grid = g, p.sell_grid = s; }
+    } restore{P, P.gather_grid, P.sell_grid};
+    P.gather_grid = std::max(1, P.gather_grid / grid_div);
+    P.sell_grid = std::max(1, P.sell_grid / grid_div);
     int have = -1;  // x chunks the compute stream already waited for (and converted)
     auto compute_chunk = [&](int c) {
         for (; have < P.hneed[c]; ++have) {

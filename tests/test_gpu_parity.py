@@ -319,6 +319,32 @@ def test_device_and_graph_entry_points():
         ex.close()
 
 
+@pytest.mark.parametrize("kind", [K.windowed, K.gather, K.atomic, K.colorful, K.local_buffers])
+@pytest.mark.parametrize("on_side_stream", [False, True])
+def test_apply_device_is_ordered_on_torch_stream(kind, on_side_stream):
+    """apply_device without a stream argument enqueues on torch's current
+    stream (the default legacy NULL stream included), so torch ops queued
+    after it see the product with no explicit synchronize in between."""
+    import torch
+    a, x, _ = P.config_matrix("c3")
+    ref = O.spmv_csrc(a, x)
+    ex = P.GpuSpmv(a, P.Strategy(kind, p=4))
+    xd = torch.from_numpy(x).cuda()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side if on_side_stream else torch.cuda.current_stream()):
+        outs = []
+        for _ in range(3):
+            y = torch.full_like(xd, float("nan"))
+            ex.apply_device(xd * 1.0, y)  # x produced by a torch op on the same stream
+            outs.append(y.clone())         # consumed by a torch op on the same stream
+            del y
+        got = torch.stack(outs).cpu().numpy()  # a copy on the same stream, no synchronize before it
+    for row in got:
+        assert rel_l2(row, ref) <= TOL64
+    ex.close()
+
+
 @pytest.mark.parametrize("cfg", ["c1", "c2"])
 @pytest.mark.parametrize("kind", [K.windowed, K.gather, K.atomic, K.colorful, K.local_buffers])
 def test_configs_full_size(cfg, kind):
