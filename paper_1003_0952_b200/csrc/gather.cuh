@@ -38,6 +38,40 @@ __device__ __forceinline__ void prefetch_span(const E* a, int64_t i0, int64_t i1
     prefetch_l2(reinterpret_cast<const void*>(b0), static_cast<uint32_t>(b1 - b0));
 }
 
+// Ordered read-only loads: volatile asm keeps the issue order of a batch of
+// independent loads (ptxas otherwise interleaves each gather with its FMA and
+// keeps only ~2 loads in flight per thread in the pattern form).
+__device__ __forceinline__ double ld_nc(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_nc(const float* p) {
+    float v;
+    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_nc(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_cs(const double* p) {
+    double v;
+    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_cs(const float* p) {
+    float v;
+    asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_cs(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
 // L lanes per row from global memory; rows = rows[0..count) when `rows` is
 // given, else row0 .. row0 + count - 1.
 template <typename T, int L, int PF>
@@ -218,6 +252,29 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     __syncthreads();
     constexpr int kIdxAlign = 4;
     constexpr int kValAlign = 16 / sizeof(T);
+    // row setup (loading the next row block's setup during the current one
+    // raised registers and cost 15-40 %: DESIGN.md §5)
+    struct RowRegs {
+        int32_t eb, ee, pb, e_base;
+        T d, xr;
+    };
+    auto load_row = [&](int64_t b, RowRegs& r) {
+        const int64_t row = b + rrel;
+        r.eb = r.ee = r.pb = r.e_base = 0;
+        r.d = r.xr = T(0);
+        if (b >= A.nrows) return;
+        r.e_base = __ldg(A.eptr + b);
+        if (row < A.nrows) {
+            r.eb = __ldg(A.eptr + row);
+            r.ee = __ldg(A.eptr + row + 1);
+            if (PAT) r.pb = __ldg(A.pbase + row) - r.eb;  // pattern slot of entry f = pb + f
+            if (A.ad) {  // CSR plans carry the diagonal in the entry stream (ad == nullptr)
+                r.d = __ldg(A.ad + row);
+                r.xr = __ldg(A.x + row);
+            }
+        }
+    };
+    RowRegs cur;
     int it = 0;
     for (int64_t base = first; base < A.nrows; base += stride, ++it) {
         const int buf = NB == 2 ? (it & 1) : 0;
@@ -227,36 +284,42 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         }
         const int64_t row = base + rrel;
         const bool act = row < A.nrows;
-        int32_t eb = 0, ee = 0, pb = 0;
-        T d = T(0), xr = T(0);
-        if (act) {
-            eb = __ldg(A.eptr + row);
-            ee = __ldg(A.eptr + row + 1);
-            if (PAT) pb = __ldg(A.pbase + row) - eb;  // pattern slot of entry f = pb + f
-            if (A.ad) {  // CSR plans carry the diagonal in the entry stream (ad == nullptr)
-                d = __ldg(A.ad + row);
-                xr = __ldg(A.x + row);
-            }
-        }
-        const int32_t e_base = __ldg(A.eptr + base);  // the row block's first entry
+        load_row(base, cur);
+        const int32_t eb = cur.eb, ee = cur.ee, pb = cur.pb, e_base = cur.e_base;
+        const T d = cur.d, xr = cur.xr;
         mbar_wait(&full[buf], NB == 2 ? ((it >> 1) & 1) : (it & 1));
         const uint32_t st = smem_u32(bufs + buf * buf_bytes);
         const uint32_t ib = st - 4u * static_cast<uint32_t>(e_base & ~(kIdxAlign - 1));
         const uint32_t vb = st + A.idx_bytes -
                             static_cast<uint32_t>(sizeof(T)) * static_cast<uint32_t>(e_base & ~(kValAlign - 1));
-        const T* xrow = A.x + row;
         const uint32_t xb = st + A.idx_bytes + A.val_bytes + static_cast<uint32_t>(sizeof(T)) * rrel;
+        const int32_t rq = static_cast<int32_t>(row);  // kernel coordinates fit int32
         T acc0 = T(0), acc1 = T(0);
         for (int32_t e = eb + sub; e < ee; e += U * L) {
             T xv[U];
+            if (XS) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int32_t f = e + u * L;
-                xv[u] = T(0);
-                if (f < ee)
-                    xv[u] = XS    ? lds_f(xb + static_cast<uint32_t>(sizeof(T)) * __ldg(A.xs_tab + pb + f), T())
-                            : PAT ? __ldg(xrow + __ldg(A.pat_off + pb + f))
-                                  : __ldg(A.x + lds_i(ib + 4u * f));
+                for (int u = 0; u < U; ++u) {
+                    const int32_t f = e + u * L;
+                    xv[u] = T(0);
+                    if (f < ee) xv[u] = lds_f(xb + static_cast<uint32_t>(sizeof(T)) * __ldg(A.xs_tab + pb + f), T());
+                }
+            } else {
+                // all U column ids, then all U gathers of x: 32-bit ids and one IMAD.WIDE per
+                // address (the 64-bit row-pointer form cost 4 integer ops per gather and
+                // 11 % at C5 fp32); volatile ordered loads measured the same as __ldg here
+                int32_t c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int32_t f = e + u * L;
+                    c[u] = rq;
+                    if (f < ee) c[u] = PAT ? rq + __ldg(A.pat_off + (pb + f)) : lds_i(ib + 4u * f);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    xv[u] = T(0);
+                    if (e + u * L < ee) xv[u] = __ldg(A.x + c[u]);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -281,39 +344,6 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     }
 }
 
-// Ordered read-only loads: volatile asm keeps the issue order of a batch of
-// independent loads (ptxas otherwise interleaves each gather with its FMA and
-// keeps only ~2 loads in flight per thread in the pattern form).
-__device__ __forceinline__ double ld_nc(const double* p) {
-    double v;
-    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float ld_nc(const float* p) {
-    float v;
-    asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ int32_t ld_nc(const int32_t* p) {
-    int32_t v;
-    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ double ld_cs(const double* p) {
-    double v;
-    asm volatile("ld.global.cs.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float ld_cs(const float* p) {
-    float v;
-    asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-}
-__device__ __forceinline__ int32_t ld_cs(const int32_t* p) {
-    int32_t v;
-    asm volatile("ld.global.cs.s32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
 
 // Sliced form (k_gather_sell, the default for mesh matrices): the entry
 // stream re-laid out in slices of H = 32 / L consecutive rows, one warp per
