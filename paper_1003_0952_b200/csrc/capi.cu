@@ -161,6 +161,7 @@ struct csrc_gpu_plan_s {
     int gather_cap = 0;    // largest entry span of a row block (k_gather_buf)
     // staged-x pattern form (k_gather_staged PF = 2)
     int gather_xs = 0;
+    int gather_rs = 0;     // row setup (eptr, pbase) staged with the values (k_gather_staged)
     int xs_clusters = 0, xs_tab_len = 0, xs_bytes = 0;
     DevBuf xs_tab, xs_clo, xs_chi, xs_cbase;
     // sliced form (k_gather_sell, default): SELL-32 layout of the entry stream
@@ -813,10 +814,17 @@ bool find_row_patterns(index_t n, const std::vector<int32_t>& eptr, const HVec<i
     return true;
 }
 
+// row-setup area per staging buffer (0 = the kernel loads eptr / pbase from global memory)
+int gather_rs_bytes(const Plan& P) {
+    if (!P.gather_rs || P.gather_xs) return 0;
+    return dev::gather_rows_bytes(P.gather_nt / P.gather_lanes) * (P.gather_pat ? 2 : 1);
+}
+
 template <class T>
 int gather_stage_smem(const Plan& P) {
     return 16 + P.gather_nb * ((P.gather_pat ? 0 : dev::gather_idx_bytes(P.gather_cap)) +
-                               dev::gather_val_bytes<T>(P.gather_cap) + (P.gather_xs ? P.xs_bytes : 0));
+                               dev::gather_val_bytes<T>(P.gather_cap) + (P.gather_xs ? P.xs_bytes : 0) +
+                               gather_rs_bytes(P));
 }
 
 // pattern form of the staged kernel: 0 explicit columns, 1 row patterns, 2 patterns + staged x
@@ -1293,6 +1301,8 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
     // dictionary of column-offset patterns
     P.gather_u = env_int("CSRC_GPU_GU", avg / P.gather_lanes <= 16 ? 8 : 4) == 8 ? 8 : 4;
     P.gather_nb = env_int("CSRC_GPU_GNB", 1) == 2 ? 2 : 1;
+    // row setup staged with the values lost 1.5-3.5 % (profiles/r01_sweep_gather_row_setup.txt): opt-in
+    P.gather_rs = env_int("CSRC_GPU_GROWS", 0) != 0 ? 1 : 0;
     {
         // 128-thread blocks (64 rows) for fp64: C5 0.631 ms vs 0.689 ms at 256 and
         // 0.664 at 64; fp32 keeps 256 (0.466 vs 0.558 ms)
@@ -1482,6 +1492,7 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
         A.x_min = P.lo - P.row_begin;  // x holds [lo, x_hi) global = these kernel coordinates
         A.x_max = P.x_hi - P.row_begin;
         A.xs_bytes = 0;
+        A.rs_bytes = gather_rs_bytes(P);
         if (P.gather_xs) {
             const int m = 16 / static_cast<int>(sizeof(T));
             const int ph = static_cast<int>((reinterpret_cast<uintptr_t>(x) / sizeof(T)) % m);

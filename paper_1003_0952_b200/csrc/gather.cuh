@@ -172,7 +172,17 @@ struct GStageArgs {
     int32_t n_clusters;
     int32_t x_min, x_max;  // readable x range (kernel coordinates)
     int32_t xs_bytes;      // x area per buffer, 16-aligned
+    // Row setup staged with the values (rs_bytes > 0): thread 0's copy also
+    // brings the row block's eptr[q0 .. q0 + R] and (PAT) pbase[q0 .. q0 + R),
+    // so a row's span is read from shared memory after the barrier wait the
+    // block makes anyway, instead of a dependent global load per row block.
+    // Measured slower (the extra small copies cost more than the load latency
+    // they hide): opt-in, CSRC_GPU_GROWS=1.
+    int32_t rs_bytes;      // row-setup area per buffer (0 = global loads)
 };
+
+// one int32 row array of a row block of R rows (+1 for eptr, + alignment pad)
+__host__ __device__ inline int gather_rows_bytes(int R) { return ((R + 8) * 4 + 15) & ~15; }
 
 // shared-memory bytes of one buffer holding up to `cap` entries (+ alignment slack)
 __host__ __device__ inline int gather_idx_bytes(int cap) { return ((cap + 8) * 4 + 15) & ~15; }
@@ -190,7 +200,9 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     const int R = blockDim.x / L;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [2]
     unsigned char* bufs = smem + 16;
-    const int buf_bytes = A.idx_bytes + A.val_bytes + (XS ? A.xs_bytes : 0);
+    const int buf_bytes = A.idx_bytes + A.val_bytes + (XS ? A.xs_bytes : 0) + A.rs_bytes;
+    const int rs_off = A.idx_bytes + A.val_bytes + (XS ? A.xs_bytes : 0);  // row-setup area in a buffer
+    const uint32_t rs_e = static_cast<uint32_t>(gather_rows_bytes(R));
     const int sub = threadIdx.x % L;
     const int rrel = threadIdx.x / L;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * R;
@@ -229,14 +241,29 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
             }
             return;
         }
+        uint32_t rs_tx = 0;
+        Seg<int32_t> se{}, sp{};
+        if (A.rs_bytes) {
+            const int64_t q1 = q0 + R < A.nrows ? q0 + R : A.nrows;
+            se = seg(A.eptr, q0, q1 + 1);
+            rs_tx = se.bytes;
+            if (PAT) {
+                sp = seg(A.pbase, q0, q1);
+                rs_tx += sp.bytes;
+            }
+        }
         if (PAT) {
-            mbar_expect_tx(&full[buf], sv.bytes);
+            mbar_expect_tx(&full[buf], sv.bytes + rs_tx);
         } else {
             const Seg<int32_t> si = seg(A.eidx, e0, e1);
-            mbar_expect_tx(&full[buf], si.bytes + sv.bytes);
+            mbar_expect_tx(&full[buf], si.bytes + sv.bytes + rs_tx);
             tma_load(st, si.src, si.bytes, &full[buf]);
         }
         tma_load(st + A.idx_bytes, sv.src, sv.bytes, &full[buf]);
+        if (A.rs_bytes) {
+            tma_load(st + rs_off, se.src, se.bytes, &full[buf]);
+            if (PAT) tma_load(st + rs_off + rs_e, sp.src, sp.bytes, &full[buf]);
+        }
     };
     if (threadIdx.x == 0) {
         mbar_init(&full[0], 1);
@@ -252,29 +279,6 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
     __syncthreads();
     constexpr int kIdxAlign = 4;
     constexpr int kValAlign = 16 / sizeof(T);
-    // row setup (loading the next row block's setup during the current one
-    // raised registers and cost 15-40 %: DESIGN.md §5)
-    struct RowRegs {
-        int32_t eb, ee, pb, e_base;
-        T d, xr;
-    };
-    auto load_row = [&](int64_t b, RowRegs& r) {
-        const int64_t row = b + rrel;
-        r.eb = r.ee = r.pb = r.e_base = 0;
-        r.d = r.xr = T(0);
-        if (b >= A.nrows) return;
-        r.e_base = __ldg(A.eptr + b);
-        if (row < A.nrows) {
-            r.eb = __ldg(A.eptr + row);
-            r.ee = __ldg(A.eptr + row + 1);
-            if (PAT) r.pb = __ldg(A.pbase + row) - r.eb;  // pattern slot of entry f = pb + f
-            if (A.ad) {  // CSR plans carry the diagonal in the entry stream (ad == nullptr)
-                r.d = __ldg(A.ad + row);
-                r.xr = __ldg(A.x + row);
-            }
-        }
-    };
-    RowRegs cur;
     int it = 0;
     for (int64_t base = first; base < A.nrows; base += stride, ++it) {
         const int buf = NB == 2 ? (it & 1) : 0;
@@ -284,11 +288,35 @@ __global__ void __launch_bounds__(256, MINB) k_gather_staged(const GStageArgs<T>
         }
         const int64_t row = base + rrel;
         const bool act = row < A.nrows;
-        load_row(base, cur);
-        const int32_t eb = cur.eb, ee = cur.ee, pb = cur.pb, e_base = cur.e_base;
-        const T d = cur.d, xr = cur.xr;
+        int32_t eb = 0, ee = 0, pb = 0, e_base = 0;
+        T d = T(0), xr = T(0);
+        if (act && A.ad) {  // CSR plans carry the diagonal in the entry stream (ad == nullptr)
+            d = __ldg(A.ad + row);
+            xr = __ldg(A.x + row);
+        }
+        if (!A.rs_bytes) {
+            e_base = __ldg(A.eptr + base);  // the row block's first entry
+            if (act) {
+                eb = __ldg(A.eptr + row);
+                ee = __ldg(A.eptr + row + 1);
+                if (PAT) pb = __ldg(A.pbase + row) - eb;  // pattern slot of entry f = pb + f
+            }
+        }
         mbar_wait(&full[buf], NB == 2 ? ((it >> 1) & 1) : (it & 1));
         const uint32_t st = smem_u32(bufs + buf * buf_bytes);
+        if (A.rs_bytes) {
+            const uint32_t ra = st + static_cast<uint32_t>(rs_off);
+            const uint32_t eo = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(A.eptr + base) & 15) >> 2);
+            e_base = lds_i(ra + 4u * eo);
+            if (act) {
+                eb = lds_i(ra + 4u * (eo + rrel));
+                ee = lds_i(ra + 4u * (eo + rrel + 1));
+                if (PAT) {
+                    const uint32_t po = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(A.pbase + base) & 15) >> 2);
+                    pb = lds_i(ra + rs_e + 4u * (po + rrel)) - eb;
+                }
+            }
+        }
         const uint32_t ib = st - 4u * static_cast<uint32_t>(e_base & ~(kIdxAlign - 1));
         const uint32_t vb = st + A.idx_bytes -
                             static_cast<uint32_t>(sizeof(T)) * static_cast<uint32_t>(e_base & ~(kValAlign - 1));

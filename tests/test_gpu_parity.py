@@ -522,6 +522,11 @@ GATHER_SHAPES = [
     {"CSRC_GPU_GNB": "2", "CSRC_GPU_GLANES": "2", "CSRC_GPU_GU": "8"},
     {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "8", "CSRC_GPU_GU": "4"},
     {"CSRC_GPU_GNB": "1", "CSRC_GPU_GLANES": "16", "CSRC_GPU_GU": "8"},
+    # row setup (eptr / pbase) staged with the values instead of global loads
+    {"CSRC_GPU_GROWS": "1"},
+    {"CSRC_GPU_GROWS": "1", "CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GNB": "2"},
+    {"CSRC_GPU_GROWS": "1", "CSRC_GPU_GLANES": "4", "CSRC_GPU_GNT": "128"},
+    {"CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GNB": "2", "CSRC_GPU_GNT": "64"},
     # sliced (SELL) form: lanes per row, steps in flight, pattern / explicit columns
     {"CSRC_GPU_GSELL": "1"},
     {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_L": "2"},
