@@ -364,7 +364,7 @@ def main():
         effective_gbs=gbs, roofline_frac_of_measured_hbm=gbs / peak,
         gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
         roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                      traffic=load_traffic(wl), peak_source=peak_src,
+                      traffic=load_traffic(wl) if world == 1 else None, peak_source=peak_src,
                       kernel=kernel_name,
                       algorithmic_bytes_per_launch=mb, kernel_ms=kms,
                       layout_bytes_per_launch=layout_bytes,

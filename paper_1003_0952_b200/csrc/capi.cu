@@ -174,8 +174,9 @@ struct csrc_gpu_plan_s {
     DevBuf sbase, rmeta, sidx, sval, sval_t;
     int gather_grid = 0;
     // host-API pipeline (apply_host): row chunks, and for each the last x chunk it reads
-    std::vector<int32_t> hchunk;
-    std::vector<int32_t> hneed;
+    std::vector<int32_t> hchunk;  // host pipeline: row chunks
+    std::vector<int32_t> hneed;   // last x chunk row chunk c reads
+    std::vector<int32_t> xchunk;  // x chunk boundaries (row-aligned, or halo-aligned)
     cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
     cudaStream_t s_h2d2 = nullptr, s_d2h2 = nullptr;  // optional second copy streams
     // pageable user vectors (std::vector in the reference's API) are staged
@@ -1285,16 +1286,33 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
         if (P.hchunk.back() != n) P.hchunk.push_back(n);
         const int nc = static_cast<int>(P.hchunk.size()) - 1;
         P.hneed.assign(nc, 0);
+        std::vector<int32_t> hi_col(nc);
         std::vector<std::thread> pool;
         for (int c = 0; c < nc; ++c)
             pool.emplace_back([&, c] {
                 int32_t hi = P.hchunk[c + 1] - 1;  // the diagonal reads x[row]
                 for (int64_t e = eptr[P.hchunk[c]]; e < eptr[P.hchunk[c + 1]]; ++e) hi = std::max(hi, eidx[e]);
-                // chunk holding column hi
-                P.hneed[c] = static_cast<int32_t>(std::upper_bound(P.hchunk.begin(), P.hchunk.end() - 1, hi) -
-                                                  P.hchunk.begin()) - 1;
+                hi_col[c] = hi;
             });
         for (auto& th : pool) th.join();
+        // x chunks: by default x chunk c ends at the highest column row chunk c
+        // reads, so chunk c's product starts once x chunk c has landed (the
+        // halo of the next rows comes with it) instead of waiting for all of
+        // x chunk c + 1; CSRC_GPU_HOST_XHALO=0 keeps x chunks = row chunks.
+        if (env_int("CSRC_GPU_HOST_XHALO", 1) != 0) {
+            P.xchunk.assign(1, 0);
+            for (int c = 0; c < nc; ++c) {
+                const int32_t e = c + 1 == nc ? static_cast<int32_t>(n)
+                                              : std::min<int32_t>(static_cast<int32_t>(n),
+                                                                  std::max(P.hchunk[c + 1], hi_col[c] + 1));
+                P.xchunk.push_back(std::max(P.xchunk.back(), e));
+            }
+        } else {
+            P.xchunk = P.hchunk;
+        }
+        for (int c = 0; c < nc; ++c)  // x chunk holding column hi
+            P.hneed[c] = static_cast<int32_t>(std::upper_bound(P.xchunk.begin(), P.xchunk.end() - 1, hi_col[c]) -
+                                              P.xchunk.begin()) - 1;
     }
     // staged form (k_gather_staged): U x-gathers in flight per lane, NB buffers,
     // NT threads per block; the row-pattern form when the rows repeat a small
@@ -1986,7 +2004,7 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         for (; have < P.hneed[c]; ++have) {
             CUDA_OK(cudaStreamWaitEvent(st, P.ev_x[have + 1], 0));
             if (f32) {
-                const int32_t a = P.hchunk[have + 1], b = P.hchunk[have + 2];
+                const int32_t a = P.xchunk[have + 1], b = P.xchunk[have + 2];
                 dev::k_convert<double, float><<<grid_for(P.device, b - a, 256), 256, 0, st>>>(
                     P.dxd.as<double>() + a, P.dx.as<float>() + a, b - a);
             }
@@ -2021,7 +2039,7 @@ void apply_host_pipelined(Plan& P, const double* xh, double* yh, bool tr) {
         }
     };
     for (int c = 0; c < nc; ++c) {
-        const size_t r0 = P.hchunk[c], len = P.hchunk[c + 1] - P.hchunk[c];
+        const size_t r0 = P.xchunk[c], len = P.xchunk[c + 1] - P.xchunk[c];
         if (xs) P.cpool->copy(P.hx_pin + r0, xh + r0, len * 8);
         cudaStream_t sc = h2d2 && (c & 1) ? P.s_h2d2 : P.s_h2d;
         CUDA_OK(cudaMemcpyAsync(xd64 + r0, xsrc + r0, len * 8, cudaMemcpyHostToDevice, sc));

@@ -1,5 +1,5 @@
 #!/bin/bash
-# round-end check: full GPU suite, smoke, bench (f64 headline + f32), reference arm
+# round-end check: full GPU suite, smoke, bench (f64 headline + f32), reference arm, launch list
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
@@ -7,3 +7,5 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"; cat gpurun_out/bench.json
 timeout 600 python bench.py --dtype f32 --no-cpu-baseline --compare "" > gpurun_out/bench_f32.json 2>> gpurun_out/bench.err; echo "bench32 rc=$?"; cat gpurun_out/bench_f32.json
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.json 2>> gpurun_out/bench.err; echo "benchref rc=$?"; cat gpurun_out/bench_ref.json
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_bench.log 2>&1; echo "launches rc=$?"; wc -l gpurun_out/launches.csv
