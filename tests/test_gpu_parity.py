@@ -491,11 +491,17 @@ def test_pageable_host_vectors(kind):
 
 
 @pytest.mark.parametrize("cfg", ["c3", "c4"])
-def test_host_pipeline_matches_device(cfg):
+@pytest.mark.parametrize("env", [{}, {"CSRC_GPU_HOST_XHALO": "0"},
+                                 {"CSRC_GPU_HOST_UNITS": "1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1,1"}])
+def test_host_pipeline_matches_device(cfg, env, monkeypatch):
     """The host entry point of a gather plan overlaps the x upload, the row
     chunks and the y download (capi.cu apply_host_pipelined); it must give
-    exactly the device entry point's result (same kernels, same order)."""
+    exactly the device entry point's result (same kernels, same order) with
+    halo-aligned x chunks (default), row-aligned x chunks, and many small
+    chunks (x chunks narrower than the halo: some come up empty)."""
     import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     a, x, _ = P.config_matrix(cfg)
     ref = O.spmv_csrc(a, x)
     for dt, tdt in ((P.DType.f64, torch.float64), (P.DType.f32, torch.float32)):

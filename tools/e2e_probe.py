@@ -29,13 +29,16 @@ xh = torch.from_numpy(x).pin_memory()
 yh = torch.empty_like(xh).pin_memory()
 schedules = ["", "1,2,4,8,8,8,8,8,8,4,2,2,1,1", "1,1,2,4,8,8,8,8,8,8,4,2,1,1,1", "2,4,8,16,16,8,4,2,2,1,1",
              "1,2,3,4,4,4,4,4,4,4,4,4,4,4,4,3,2,1,1", "4,8,8,8,8,8,8,8,4,2,2,1,1"]
+if len(sys.argv) > 2:  # schedules given as ';'-separated unit lists ('' = the default)
+    schedules = sys.argv[2].split(";")
+streams = ((1, 1), (2, 1), (1, 2), (2, 2)) if len(sys.argv) <= 3 else ((1, 1),)
 for sch in schedules:
     if sch:
         os.environ["CSRC_GPU_HOST_UNITS"] = sch
     else:
         os.environ.pop("CSRC_GPU_HOST_UNITS", None)
     ex = P.GpuSpmv(a, P.Strategy(P.StrategyKind.gather))
-    for h2, d2 in ((1, 1), (2, 1), (1, 2), (2, 2)):
+    for h2, d2 in streams:
         os.environ["CSRC_GPU_HOST_H2D_STREAMS"] = str(h2)
         os.environ["CSRC_GPU_HOST_D2H_STREAMS"] = str(d2)
         t = timeit(lambda: ex.apply(xh.numpy(), yh.numpy()))
