@@ -861,6 +861,9 @@ template <class T>
 void* gather_stage_fn(const Plan& P) {
     const int pf = gather_pf(P);
     switch (P.gather_lanes) {
+        case 1:  // one row per thread: U = 8, one buffer, no min-blocks bound, no staged x (setup_gather)
+            return pf == 1 ? reinterpret_cast<void*>(&dev::k_gather_staged<T, 1, 8, 1, 1, 1>)
+                           : reinterpret_cast<void*>(&dev::k_gather_staged<T, 1, 8, 1, 0, 1>);
         case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, pf, P.gather_minb);
         case 8: return gather_stage_fn_L<T, 8>(P.gather_u, P.gather_nb, pf, P.gather_minb);
         default: return gather_stage_fn_L<T, 4>(P.gather_u, P.gather_nb, pf, P.gather_minb);
@@ -1246,7 +1249,9 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
         t_last = t;
     };
     const double avg = n ? static_cast<double>(ne) / n : 0.0;
-    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? 2 : avg <= 128 ? 4 : 8);
+    // lanes per row: stencil rows (<= 40 entries) 2 for fp64, 1 for fp32 (C5 fp32
+    // 0.422 vs 0.470 ms; fp64 0.631 vs 0.747 ms with 1: profiles/r01_sweep_gather_one_lane.txt)
+    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? (sizeof(T) == 4 ? 1 : 2) : avg <= 128 ? 4 : 8);
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
     P.gather_bpsm = env_int("CSRC_GPU_GBPSM", 16);  // 256-thread blocks per SM
     if (!band) {
@@ -1337,10 +1342,18 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
     const bool has_pat = P.gather_lanes <= 8 && find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns);
     mark("row patterns");
     P.gather_pat = has_pat && env_int("CSRC_GPU_GPATTERN", 1) != 0 ? 1 : 0;
-    if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 2 && P.gather_lanes <= 8) {
+    if (env_int("CSRC_GPU_GBUF", 1) != 0 && P.gather_lanes >= 1 && P.gather_lanes <= 8) {
         const int R = P.gather_nt / P.gather_lanes;
+        if (P.gather_lanes == 1) {  // the one instantiated one-row-per-thread shape (gather_stage_fn)
+            P.gather_u = 8;
+            P.gather_nb = 1;
+            P.gather_minb = 1;
+        }
         // staged x (pattern form): x windows of each row block come in by TMA with the values
-        P.gather_xs = P.gather_pat && env_int("CSRC_GPU_GXS", 0) != 0 && setup_staged_x<T>(P, pat_off) ? 1 : 0;
+        P.gather_xs = P.gather_pat && P.gather_lanes >= 2 && env_int("CSRC_GPU_GXS", 0) != 0 &&
+                              setup_staged_x<T>(P, pat_off)
+                          ? 1
+                          : 0;
         int64_t cap = 0;
         for (int64_t b = 0; b < n; b += R) cap = std::max<int64_t>(cap, eptr[std::min<int64_t>(n, b + R)] - eptr[b]);
         if (cap <= 16384) {

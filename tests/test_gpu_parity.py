@@ -533,6 +533,9 @@ GATHER_SHAPES = [
     {"CSRC_GPU_GROWS": "1", "CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GNB": "2"},
     {"CSRC_GPU_GROWS": "1", "CSRC_GPU_GLANES": "4", "CSRC_GPU_GNT": "128"},
     {"CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GNB": "2", "CSRC_GPU_GNT": "64"},
+    # staged, one row per thread
+    {"CSRC_GPU_GLANES": "1"},
+    {"CSRC_GPU_GLANES": "1", "CSRC_GPU_GPATTERN": "0", "CSRC_GPU_GNT": "128"},
     # sliced (SELL) form: lanes per row, steps in flight, pattern / explicit columns
     {"CSRC_GPU_GSELL": "1"},
     {"CSRC_GPU_GSELL": "1", "CSRC_GPU_SELL_L": "2"},
