@@ -861,7 +861,8 @@ template <class T>
 void* gather_stage_fn(const Plan& P) {
     const int pf = gather_pf(P);
     switch (P.gather_lanes) {
-        case 1:  // one row per thread: U = 8, one buffer, no min-blocks bound, no staged x (setup_gather)
+        case 1:  // one row per thread: U = 8, one buffer, no staged x (setup_gather); opt-in 6-block bound
+            if (pf == 1 && P.gather_minb == 6) return reinterpret_cast<void*>(&dev::k_gather_staged<T, 1, 8, 1, 1, 6>);
             return pf == 1 ? reinterpret_cast<void*>(&dev::k_gather_staged<T, 1, 8, 1, 1, 1>)
                            : reinterpret_cast<void*>(&dev::k_gather_staged<T, 1, 8, 1, 0, 1>);
         case 2: return gather_stage_fn_L<T, 2>(P.gather_u, P.gather_nb, pf, P.gather_minb);
@@ -1347,7 +1348,11 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
         if (P.gather_lanes == 1) {  // the one instantiated one-row-per-thread shape (gather_stage_fn)
             P.gather_u = 8;
             P.gather_nb = 1;
-            P.gather_minb = 1;
+            // fp32: a 6-block bound (40 registers, no spills) over the unbounded 43-register form,
+            // C5 0.415 vs 0.424 ms, C3/C4 unchanged (profiles/r01_sweep_gather_minb_l1.txt);
+            // CSRC_GPU_GMINB=1 restores the unbounded form
+            const int mb1 = env_int("CSRC_GPU_GMINB", sizeof(T) == 4 ? 6 : 1);
+            P.gather_minb = mb1 == 6 ? 6 : 1;
         }
         // staged x (pattern form): x windows of each row block come in by TMA with the values
         P.gather_xs = P.gather_pat && P.gather_lanes >= 2 && env_int("CSRC_GPU_GXS", 0) != 0 &&
