@@ -111,62 +111,120 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_reference(a, x, seconds, threads, sample_reps=None):
-    """Reference CPU path timed on this host: oracle/_ref ParallelSpmv
-    (interval accumulation, p = host threads) when built, else the plain-C
-    oracle port (single thread). Returns dict(value_gflops, ...)."""
-    from oracle.oracle import Oracle, Ref
+REF_METHODS = [("sequential", 0, 0), ("all_in_one", 1, 0), ("per_buffer", 1, 1), ("effective", 1, 2),
+               ("interval", 1, 3)]
+
+
+def cpu_reference_suite(a, x, seconds, ref_threads=None):
+    """The reference's own CPU path timed on this host:
+    sequential spmv_csrc (kernels.hpp:25-43, via ParallelSpmv p=1, parallel.hpp:197-202)
+    and ParallelSpmv local buffers x {all_in_one, per_buffer, effective, interval}
+    (parallel.hpp:309-397) at p = the physical cores this process may use, from
+    oracle/_ref (compiled from /root/reference for the host's x86-64 ISA level).
+    Colorful is not timed: the reference's std::set conflict graph does not fit at
+    C3-C5 (34 GB / 371 s exact, > 62 GB neighbourhood at C5).
+    Falls back to the plain-C oracle port (1 thread) where oracle/_ref is absent.
+    Each method: one warm product, then a bounded sample of products (median of 3
+    runs, bench.hpp:125-128). Returns a dict; `best` names the fastest method."""
+    from oracle.oracle import Oracle, Ref, host_cores
     flops = 2 * a.nnz_full()
+    hc = host_cores()
+    p = ref_threads or max(1, hc["physical"])
+    methods = {}
     if Ref.available():
         R = Ref()
-        h = R.exec_create(a, 1, 3, threads)  # local_buffers, interval (fastest, SURVEY.md 6)
-        dt1, y, _ = R.exec_run(h, x, 1, a.n)  # warm
-        reps = sample_reps or max(1, min(500, int(seconds / max(dt1, 1e-6))))
-        dt, y, ph = R.exec_run(h, x, reps, a.n)
-        R.exec_destroy(h)
-        return dict(value=flops * reps / dt / 1e9, kind="reference", cores=threads, reps=reps,
-                    seconds=dt, y=y,
-                    sample=f"{reps} products of the full workload, reference ParallelSpmv "
-                           f"(local_buffers/interval, p={threads}), oracle/_ref built from /root/reference")
-    O = Oracle()
-    t0 = time.perf_counter()
-    y = O.spmv_csrc(a, x)
-    dt1 = time.perf_counter() - t0
-    reps = sample_reps or max(1, min(200, int(seconds / max(dt1, 1e-6))))
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        y = O.spmv_csrc(a, x)
-    dt = time.perf_counter() - t0
-    return dict(value=flops * reps / dt / 1e9, kind="port", cores=1, reps=reps, seconds=dt, y=y,
-                sample=f"{reps} products of the full workload, plain-C oracle port of spmv_csrc (1 thread)")
+        per = seconds / len(REF_METHODS)
+        for name, kind, accum in REF_METHODS:
+            h = R.exec_create(a, kind, accum, 1 if kind == 0 else p)
+            try:
+                dt1, y, _ = R.exec_run(h, x, 1, a.n)  # warm (first touch of the buffers)
+                reps = max(1, min(1000, int(per / 3 / max(dt1, 1e-6))))
+                runs = []
+                for _ in range(3 if dt1 * reps * 3 <= per * 1.5 else 1):
+                    dt, y, ph = R.exec_run(h, x, reps, a.n)
+                    runs.append((dt / reps, ph / reps))
+                runs.sort(key=lambda r: r[0])
+                t, ph = runs[len(runs) // 2]
+            finally:
+                R.exec_destroy(h)
+            methods[name] = dict(ms=t * 1e3, gflops=flops / t / 1e9, p=1 if kind == 0 else p, reps=reps,
+                                 runs=len(runs), init_ms=ph[0] * 1e3, compute_ms=ph[1] * 1e3,
+                                 accumulate_ms=ph[2] * 1e3)
+        kind_s, lib = "reference", os.path.relpath(R.so, ROOT)
+    else:
+        O = Oracle()
+        t0 = time.perf_counter()
+        O.spmv_csrc(a, x)
+        dt1 = time.perf_counter() - t0
+        reps = max(1, min(200, int(seconds / max(dt1, 1e-6))))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            O.spmv_csrc(a, x)
+        t = (time.perf_counter() - t0) / reps
+        methods["sequential"] = dict(ms=t * 1e3, gflops=flops / t / 1e9, p=1, reps=reps, runs=1)
+        kind_s, lib, p = "port", "oracle/_build/libcsrc_oracle.so", 1
+    best = max(methods, key=lambda m: methods[m]["gflops"])
+    return dict(value=methods[best]["gflops"], best=best, methods=methods, kind=kind_s, lib=lib,
+                cores=methods[best]["p"], host=hc,
+                seq_gflops=methods.get("sequential", {}).get("gflops"))
+
+
+def oracle_side_fixture(args):
+    """The workload from the standalone fixture generator (oracle/_build/
+    libcsrc_fixtures.so): the reference arm never maps the product library."""
+    from oracle.oracle import config_fixture, working_set_bytes
+    a, x = config_fixture(args.config)
+    if args.dtype == "f32":  # the reference is fp64-only (common.hpp:20): fp32-rounded inputs
+        for f in ("ad", "al", "au"):
+            setattr(a, f, getattr(a, f).astype(np.float32).astype(np.float64))
+        x = x.astype(np.float32).astype(np.float64)
+    mb = working_set_bytes(a.n, a.nnz_stored(), a.value_symmetric, f32=args.dtype == "f32")
+    return a, x, mb
 
 
 def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's own CPU implementation of the path
+    (oracle/_ref, compiled from /root/reference) on this host's cores, same
+    workload, metric and unit. Rank 0 only under torchrun."""
     if world > 1 and rank != 0:
         return 0
-    import paper_1003_0952_b200 as P
-    a, x, _ = P.config_matrix(args.config)
-    if args.dtype == "f32":
-        a = P.CsrcMatrix(a.n, a.ad.astype(np.float32).astype(np.float64), a.ia, a.ja,
-                         a.al.astype(np.float32).astype(np.float64),
-                         a.au.astype(np.float32).astype(np.float64))
-        x = x.astype(np.float32).astype(np.float64)
-    threads = os.cpu_count() or 1
-    from oracle.oracle import Oracle, Ref
+    from oracle.oracle import Ref, Oracle, host_cores
+    a, x, mb = oracle_side_fixture(args)
+    flops = 2 * a.nnz_full()
+    hc = host_cores()
+    p = max(1, hc["physical"])
     per_step = []
+    suite = None
     if Ref.available():
         R = Ref()
-        h = R.exec_create(a, 1, 3, threads)  # ParallelSpmv local_buffers/interval, p = host threads
+        # pick the reference's fastest method on this host (one product each), then time it
+        probe = {}
+        for name, kind, accum in REF_METHODS:
+            h = R.exec_create(a, kind, accum, 1 if kind == 0 else p)
+            try:
+                R.exec_run(h, x, 1, a.n)
+                dt, _, _ = R.exec_run(h, x, 1, a.n)
+            finally:
+                R.exec_destroy(h)
+            probe[name] = dict(ms=dt * 1e3, gflops=flops / dt / 1e9)
+        best = min(probe, key=lambda m: probe[m]["ms"])
+        kind, accum = [(k, ac) for n, k, ac in REF_METHODS if n == best][0]
+        p_best = 1 if kind == 0 else p
+        h = R.exec_create(a, kind, accum, p_best)
         dt1, _, _ = R.exec_run(h, x, 1, a.n)
-        reps = max(1, int(args.ref_seconds / args.steps / max(dt1, 1e-6)))
+        reps = max(1, int(args.ref_seconds / max(args.steps, 1) / max(dt1, 1e-6)))
         for i in range(args.warmup + args.steps):
             dt, _, _ = R.exec_run(h, x, reps if i >= args.warmup else 1, a.n)
             if i >= args.warmup:
                 per_step.append(dt / reps)
         R.exec_destroy(h)
-        res = dict(kind="reference", cores=threads,
-                   sample=f"each step = {reps} products of the full workload through the reference "
-                          f"ParallelSpmv (local_buffers/interval, p={threads}, oracle/_ref)")
+        what = "sequential spmv_csrc" if kind == 0 else f"ParallelSpmv(local_buffers/{best}, p={p} physical cores)"
+        res = dict(kind="reference", cores=p_best, lib=os.path.relpath(R.so, ROOT),
+                   sample=f"each step = {reps} products of the full workload through the reference's {what}, "
+                          f"the fastest of its sequential path and four accumulations on this host "
+                          f"(one-product probe: methods); {os.path.relpath(R.so, ROOT)} compiled from "
+                          f"/root/reference")
+        suite = probe
     else:
         O = Oracle()
         for i in range(args.warmup + args.steps):
@@ -174,32 +232,49 @@ def run_reference_arm(args, world, rank):
             O.spmv_csrc(a, x)
             if i >= args.warmup:
                 per_step.append(time.perf_counter() - t0)
-        res = dict(kind="port", cores=1, sample="each step = 1 product, plain-C oracle port (1 thread)")
+        res = dict(kind="port", cores=1, lib="oracle/_build/libcsrc_oracle.so",
+                   sample="each step = 1 product, plain-C oracle port of spmv_csrc (1 thread)")
     ms = 1e3 * statistics.median(per_step)
-    flops = 2 * a.nnz_full()
     value = flops / (ms / 1e3) / 1e9
-    mb = P.model_bytes(a, P.DType.f32 if args.dtype == "f32" else P.DType.f64)
     line = dict(
         metric=METRIC, value=value, unit="GFLOP/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
-        ms_per_step=ms, higher_is_better=True, scaling="strong",
+        ms_per_step=ms, higher_is_better=True, scaling=bench_scaling(args),
         vs_baseline=None, dtype=args.dtype, data="synthetic",
-        config=workload_config(args, a, world), impl="reference",
+        config=workload_config_plain(args, a, mb, world), impl="reference",
         effective_gbs=mb / (ms / 1e3) / 1e9,
         cpu_baseline=dict(value=value, unit="GFLOP/s", cores=res["cores"], kind=res["kind"],
-                          sample=res["sample"]),
+                          sample=res["sample"], host=hc, methods=suite, lib=res["lib"]),
         e2e=dict(value=value, unit="GFLOP/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
     )
     print(json.dumps(line), flush=True)
     return 0
 
 
+CONFIG_DESC = {
+    "c1": "2D Q1 256x256, 9-point, seed 42",
+    "c2": "3D 64^3, 27-point, seed 7",
+    "c3": "3D 160^3, 27-point, permuted (seed 11) + RCM",
+    "c4": "elasticity 96^3 x 3 dof, 81-entry rows, seed 3",
+    "c5": "3D 256^3, 27-point, seed 99",
+}
+
+
+def bench_scaling(args):
+    # N > 1: the same matrix split into N row bands (total work fixed as N grows)
+    return "strong"
+
+
+def workload_config_plain(args, a, mb, world):
+    return {"workload": f"{args.config}: {CONFIG_DESC[args.config]}, {args.dtype}", "n": a.n,
+            "nnz": a.nnz_full(), "pairs": a.k_off(), "kind": args.kind,
+            "parallelism": f"row bands x{world}" if world > 1 else "1 GPU",
+            "l2": "working set > 126 MB L2 (no flush needed)" if mb > 400e6
+            else f"L2 flushed between steps ({args.flush_mb} MB write)"}
+
+
 def workload_config(args, a, world):
     import paper_1003_0952_b200 as P
-    c = P.CONFIGS[args.config]
-    return {"workload": f"{args.config}: {c['desc']}, {args.dtype}", "n": a.n, "nnz": a.nnz_full(),
-            "pairs": a.k_off(), "kind": args.kind, "parallelism": f"row bands x{world}" if world > 1 else "1 GPU",
-            "l2": "working set > 126 MB L2 (no flush needed)" if P.model_bytes(a) > 400e6
-            else f"L2 flushed between steps ({args.flush_mb} MB write)"}
+    return workload_config_plain(args, a, P.model_bytes(a), world)
 
 
 def main():
@@ -216,6 +291,7 @@ def main():
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample budget")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
@@ -379,10 +455,16 @@ def main():
     if others:
         line["kernels"] = others
     if world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        res = cpu_reference(a if args.dtype == "f64" else a, x, 15.0, threads)
-        line["cpu_baseline"] = dict(value=res["value"], unit="GFLOP/s", cores=res["cores"], kind=res["kind"],
-                                    sample=res["sample"])
+        a_c, x_c, _ = oracle_side_fixture(args)
+        res = cpu_reference_suite(a_c, x_c, args.cpu_seconds)
+        del a_c, x_c
+        line["cpu_baseline"] = dict(
+            value=res["value"], unit="GFLOP/s", cores=res["cores"], kind=res["kind"],
+            sample=(f"the full workload, median of up to 3 runs of a bounded product count per method "
+                    f"({args.cpu_seconds:.0f} s total); value = the fastest method ({res['best']}, "
+                    f"p = {res['cores']} of {res['host']['physical']} physical cores / "
+                    f"{res['host']['logical']} logical CPUs); {res['lib']}"),
+            methods=res["methods"], sequential_gflops=res["seq_gflops"], host=res["host"])
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

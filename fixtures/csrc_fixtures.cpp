@@ -1,5 +1,8 @@
 // Deterministic synthetic FE matrices for the BASELINE.json configs,
 // assembled directly in CSRC form (no triplet sort), multithreaded.
+// Test / bench INPUT definitions: compiled into the
+// product library (csrc_bench --config, P.config_matrix) and, standalone, into
+// oracle/_build/libcsrc_fixtures.so for the reference arm.
 //
 // The reference can only generate dense / band / random patterns
 // (generate.hpp:12-65); these meshes are the fixture definitions of
@@ -16,7 +19,40 @@
 #include <numeric>
 #include <thread>
 
-#include "internal.hpp"
+#ifdef CSRC_FIXTURES_STANDALONE
+// Standalone build (oracle/Makefile -> oracle/_build/libcsrc_fixtures.so): the
+// reference arm of bench.py and the oracle-side tests generate their inputs
+// without mapping the product library. Same source, same matrices.
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../include/csrc_gpu.h"
+
+namespace csrcgpu {
+struct Error : std::runtime_error {
+    explicit Error(const std::string& m) : std::runtime_error(m) {}
+};
+thread_local std::string g_fixture_error;
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::exception& e) {
+        g_fixture_error = e.what();
+        return 1;
+    } catch (...) {
+        g_fixture_error = "unknown error";
+        return 1;
+    }
+}
+}  // namespace csrcgpu
+extern "C" const char* csrc_fixture_last_error(void) { return csrcgpu::g_fixture_error.c_str(); }
+#else
+#include "../paper_1003_0952_b200/csrc/internal.hpp"
+#endif
 
 namespace csrcgpu {
 namespace {

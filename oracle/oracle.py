@@ -26,7 +26,67 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libcsrc_oracle.so")
-REF_SO = os.path.join(HERE, "_ref", "libcsrc_ref.so")
+FIXTURES_SO = os.path.join(HERE, "_build", "libcsrc_fixtures.so")
+
+
+def host_isa_level() -> int:
+    """x86-64 micro-architecture level (2, 3 or 4) of the CPU this process runs
+    on, from /proc/cpuinfo flags. Stands in for -march=native: the reference is
+    compiled here once per level (oracle/Makefile) and loaded at the host's."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    fl = set(line.split(":", 1)[1].split())
+                    break
+            else:
+                return 2
+    except OSError:
+        return 2
+    v3 = {"avx", "avx2", "bmi1", "bmi2", "f16c", "fma", "movbe", "abm", "xsave"}
+    v4 = {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"}
+    if v3 <= fl:
+        return 4 if v4 <= fl else 3
+    return 2
+
+
+def _ref_so() -> str:
+    lvl = host_isa_level()
+    for l in range(lvl, 1, -1):
+        p = os.path.join(HERE, "_ref", "libcsrc_ref.so" if l == 2 else f"libcsrc_ref_v{l}.so")
+        if os.path.exists(p):
+            return p
+    return os.path.join(HERE, "_ref", "libcsrc_ref.so")
+
+
+REF_SO = _ref_so()
+
+
+def host_cores() -> dict:
+    """Logical CPUs this process may run on and the physical cores behind them
+    (sysfs topology: distinct (package, core) pairs of the allowed CPUs)."""
+    cpus = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(range(os.cpu_count() or 1))
+    phys = set()
+    for c in cpus:
+        base = f"/sys/devices/system/cpu/cpu{c}/topology/"
+        try:
+            with open(base + "physical_package_id") as f:
+                pk = f.read().strip()
+            with open(base + "core_id") as f:
+                co = f.read().strip()
+            phys.add((pk, co))
+        except OSError:
+            phys.add(("?", str(c)))
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return dict(logical=len(cpus), physical=len(phys), model=model, isa_level=host_isa_level())
 
 P_i32 = C.POINTER(C.c_int32)
 P_i64 = C.POINTER(C.c_int64)
@@ -207,6 +267,7 @@ class Ref:
     def __init__(self):
         if not os.path.exists(REF_SO):
             raise FileNotFoundError(REF_SO)
+        self.so = REF_SO
         self.lib = C.CDLL(REF_SO)
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
@@ -436,6 +497,88 @@ class Ref:
 
     def working_set_kb(self, n, nnz, vs):
         return float(self.lib.ref_working_set_kb(n, nnz, int(vs)))
+
+
+# ------------------------------------------------- fixtures without the product
+class CpuCsrc:
+    """Plain CSRC arrays (the csrc::CsrcMatrix fields) for the oracle side."""
+
+    def __init__(self, n, ad, ia, ja, al, au, value_symmetric=False):
+        self.n, self.ad, self.ia, self.ja, self.al, self.au = int(n), ad, ia, ja, al, au
+        self.value_symmetric = bool(value_symmetric)
+
+    def k_off(self):
+        return int(self.ja.size)
+
+    def nnz_full(self):
+        return self.n + 2 * self.k_off()
+
+    def nnz_stored(self):
+        return self.n + (1 if self.value_symmetric else 2) * self.k_off()
+
+
+# BASELINE.json configs (the same definitions as paper_1003_0952_b200.CONFIGS,
+# checked equal in tests/test_oracle.py): mesh, nx, ny, nz, seed, diag_base
+ORACLE_CONFIGS = {
+    "c1": (0, 256, 256, 1, 42, 10.0),
+    "c2": (1, 64, 64, 64, 7, 30.0),
+    "c3": (3, 160, 160, 160, 11, 30.0),
+    "c4": (2, 96, 96, 96, 3, 100.0),
+    "c5": (1, 256, 256, 256, 99, 30.0),
+}
+
+
+class _FixtureSpec(C.Structure):
+    _fields_ = [("mesh", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
+                ("seed", C.c_uint64), ("diag_base", C.c_double), ("threads", C.c_int32)]
+
+
+class _HostMatrix(C.Structure):
+    _fields_ = [("n", C.c_int32), ("k", C.c_int64), ("ad", P_f64), ("ia", P_i32), ("ja", P_i32),
+                ("al", P_f64), ("au", P_f64), ("value_symmetric", C.c_int32)]
+
+
+def fixture(mesh, nx, ny, nz, seed, diag_base, threads=0):
+    """The seeded fixture from the standalone generator
+    oracle/_build/libcsrc_fixtures.so (fixtures/csrc_fixtures.cpp) -- the
+    reference arm and oracle-side code never map the product library.
+    Returns (CpuCsrc, x)."""
+    if not os.path.exists(FIXTURES_SO):
+        build_oracle()
+    lib = C.CDLL(FIXTURES_SO)
+    lib.csrc_fixture_generate.argtypes = [C.POINTER(_FixtureSpec), C.POINTER(C.c_void_p)]
+    lib.csrc_fixture_matrix.argtypes = [C.c_void_p, C.POINTER(_HostMatrix)]
+    lib.csrc_fixture_x.restype = P_f64
+    lib.csrc_fixture_x.argtypes = [C.c_void_p]
+    lib.csrc_fixture_free.argtypes = [C.c_void_p]
+    lib.csrc_fixture_last_error.restype = C.c_char_p
+    spec = _FixtureSpec(int(mesh), nx, ny, nz, seed, diag_base, threads)
+    h = C.c_void_p()
+    if lib.csrc_fixture_generate(C.byref(spec), C.byref(h)):
+        raise ValueError(lib.csrc_fixture_last_error().decode())
+    try:
+        m = _HostMatrix()
+        lib.csrc_fixture_matrix(h, C.byref(m))
+        n, k = m.n, m.k
+        cp = lambda q, cnt: np.ctypeslib.as_array(q, shape=(cnt,)).copy() if cnt else np.zeros(0, q._type_)  # noqa
+        a = CpuCsrc(n, cp(m.ad, n), cp(m.ia, n + 1), cp(m.ja, k), cp(m.al, k), cp(m.au, k), False)
+        x = cp(lib.csrc_fixture_x(h), n)
+    finally:
+        lib.csrc_fixture_free(h)
+    return a, x
+
+
+def config_fixture(name, threads=0):
+    return fixture(*ORACLE_CONFIGS[name], threads=threads)
+
+
+def working_set_bytes(n, nnz_stored, value_symmetric=False, f32=False):
+    """working_set_kb (working_set.hpp:17-25) in bytes: 8(ad+al+au+x+y) + 4(ia+ja)
+    for f64 values; f32 values: 4 per value."""
+    k = (nnz_stored - n) // (1 if value_symmetric else 2)
+    vb = 4 if f32 else 8
+    vals = n + (1 if value_symmetric else 2) * k
+    return vb * (vals + 2 * n) + 4 * (n + 1 + k)
 
 
 # ------------------------------------------------- fixture restatement (numpy)

@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <thread>
@@ -62,7 +64,10 @@ void upload(DevBuf& d, const U* h, size_t count) {
     if (!count) return;
     const size_t bytes = count * sizeof(U);
     if (bytes < (size_t(64) << 20)) {
-        CUDA_OK(cudaMemcpy(d.p, h, bytes, cudaMemcpyHostToDevice));
+        // legacy-stream copy + sync: a pageable cudaMemcpy may return before its DMA lands,
+        // and the plan's kernels run on non-blocking streams
+        CUDA_OK(cudaMemcpyAsync(d.p, h, bytes, cudaMemcpyHostToDevice, cudaStreamLegacy));
+        CUDA_OK(cudaStreamSynchronize(cudaStreamLegacy));
         return;
     }
     // large plan arrays: pinned staging + parallel memcpy (hostlink.cuh)
@@ -95,6 +100,23 @@ int pow2_at_least(int64_t v) {
     int64_t p = 1;
     while (p < v) p <<= 1;
     return static_cast<int>(p);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize belongs to the kernel function, not to a
+// plan: every launch sets it for its own size (plans of one shape share the function).
+// The limit only ever rises (a per-function high-water mark), so concurrent plans on
+// other host threads can never lower it between another plan's set and launch.
+void set_smem_limit(const void* fn, int smem) {
+    if (smem <= 48 * 1024) return;
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> high;  // (function, device) -> limit
+    int dev = 0;
+    CUDA_OK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    int& h = high[{fn, dev}];
+    if (smem <= h) return;
+    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    h = smem;
 }
 
 int num_sms(int device) {
@@ -206,6 +228,9 @@ struct csrc_gpu_plan_s {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     bool ev_recorded = false;
 
+    // ordering of caller streams against the plan's own stream (plan scratch users)
+    cudaEvent_t ev_join[2] = {nullptr, nullptr};
+
     // graph cache
     cudaGraphExec_t graph = nullptr;
     const void* g_x = nullptr;
@@ -237,6 +262,8 @@ struct csrc_gpu_plan_s {
             for (auto& e : *v)
                 if (e) cudaEventDestroy(e);
         if (ev_in) cudaEventDestroy(ev_in);
+        for (auto& e : ev_join)
+            if (e) cudaEventDestroy(e);
         if (s_h2d) cudaStreamDestroy(s_h2d);
         if (s_d2h) cudaStreamDestroy(s_d2h);
         if (s_h2d2) cudaStreamDestroy(s_h2d2);
@@ -476,8 +503,7 @@ auto windowed_fn(int L, int TR, bool rings) {
 template <class T>
 int windowed_blocks_per_sm(const Plan& P, size_t smem) {
     auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows, P.win_ring);
-    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+    set_smem_limit(reinterpret_cast<const void*>(fn), static_cast<int>(smem));
     int nb = 0;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 32 + P.tile_rows * P.win_lanes,
                                                          smem));
@@ -1008,7 +1034,7 @@ void setup_sell(Plan& P, index_t n, const std::vector<int32_t>& eptr, const HVec
     P.sell_pat_len = pat ? static_cast<int>(pat_off.size()) : 0;
     void* fn = sell_fn<T>(P);
     const int smem = 4 * P.sell_pat_len;
-    if (smem > 48 * 1024) CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    set_smem_limit(reinterpret_cast<const void*>(fn), smem);
     int occ = 0;
     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
     const int64_t blocks = (ns + 7) / 8;
@@ -1252,7 +1278,12 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
     const double avg = n ? static_cast<double>(ne) / n : 0.0;
     // lanes per row: stencil rows (<= 40 entries) 2 for fp64, 1 for fp32 (C5 fp32
     // 0.422 vs 0.470 ms; fp64 0.631 vs 0.747 ms with 1: profiles/r01_sweep_gather_one_lane.txt)
-    P.gather_lanes = env_int("CSRC_GPU_GLANES", avg <= 40 ? (sizeof(T) == 4 ? 1 : 2) : avg <= 128 ? 4 : 8);
+    {
+        const int dflt = avg <= 40 ? (sizeof(T) == 4 ? 1 : 2) : avg <= 128 ? 4 : 8;
+        const int l = env_int("CSRC_GPU_GLANES", dflt);
+        // only the instantiated lane counts: R = nt / lanes must match the kernel's own
+        P.gather_lanes = (l == 1 || l == 2 || l == 4 || l == 8 || l == 16) ? l : dflt;
+    }
     P.gather_pf = env_int("CSRC_GPU_GPF", 0);
     P.gather_bpsm = env_int("CSRC_GPU_GBPSM", 16);  // 256-thread blocks per SM
     if (!band) {
@@ -1334,10 +1365,8 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
         const int nt = env_int("CSRC_GPU_GNT", sizeof(T) == 8 ? 128 : 256);
         P.gather_nt = (nt == 64 || nt == 128) ? nt : 256;
     }
-    {
-        const int mb = env_int("CSRC_GPU_GMINB", 1);
-        P.gather_minb = (mb == 8 || mb == 6 || mb == 5) ? mb : 1;
-    }
+    const int minb_env = env_int("CSRC_GPU_GMINB", -1);  // read once; -1 = per-shape default
+    P.gather_minb = (minb_env == 8 || minb_env == 6 || minb_env == 5) ? minb_env : 1;
     mark("host pipeline chunks");
     std::vector<int32_t> pbase, pat_off;
     const bool has_pat = P.gather_lanes <= 8 && find_row_patterns(n, eptr, eidx, pbase, pat_off, &P.n_patterns);
@@ -1351,8 +1380,8 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
             // fp32: a 6-block bound (40 registers, no spills) over the unbounded 43-register form,
             // C5 0.415 vs 0.424 ms, C3/C4 unchanged (profiles/r01_sweep_gather_minb_l1.txt);
             // CSRC_GPU_GMINB=1 restores the unbounded form
-            const int mb1 = env_int("CSRC_GPU_GMINB", sizeof(T) == 4 ? 6 : 1);
-            P.gather_minb = mb1 == 6 ? 6 : 1;
+            const int mb1 = minb_env < 0 ? (sizeof(T) == 4 ? 6 : 1) : minb_env;
+            P.gather_minb = mb1 == 6 ? 6 : 1;  // the instantiated bounds of this shape
         }
         // staged x (pattern form): x windows of each row block come in by TMA with the values
         P.gather_xs = P.gather_pat && P.gather_lanes >= 2 && env_int("CSRC_GPU_GXS", 0) != 0 &&
@@ -1366,7 +1395,7 @@ void finish_gather(Plan& P, index_t n, bool band, std::vector<int32_t>& eptr, HV
             const int smem = gather_stage_smem<T>(P);
             if (smem <= 100 * 1024) {
                 void* fn = gather_stage_fn<T>(P);
-                CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                set_smem_limit(reinterpret_cast<const void*>(fn), smem);
                 // shared/L1 split: the driver's choice by default (L1 serves the x gathers)
                 const int carve = env_int("CSRC_GPU_GCARVE", -1);
                 if (carve >= 0)
@@ -1502,6 +1531,9 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
         const int64_t blocks = (static_cast<int64_t>(A.slice1 - A.slice0) + 7) / 8;
         const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks, P.sell_grid)));
         void* args[] = {&A};
+        // the smem limit is an attribute of the kernel instantiation, shared by every plan of
+        // this shape: set it per launch so a smaller plan created later cannot lower it
+        set_smem_limit(sell_fn<T>(P), 4 * P.sell_pat_len);
         CUDA_OK(cudaLaunchKernel(sell_fn<T>(P), dim3(grid), dim3(256), args, static_cast<size_t>(4 * P.sell_pat_len),
                                  st));
         return;
@@ -1542,6 +1574,7 @@ void launch_gather_range(const Plan& P, bool tr, const T* x, T* y, int32_t r0, i
         const int64_t blocks = (static_cast<int64_t>(r1 - r0) + R - 1) / R;
         const int grid = static_cast<int>(std::min<int64_t>(blocks, P.gather_grid));
         void* args[] = {&A};
+        set_smem_limit(gather_stage_fn<T>(P), gather_stage_smem<T>(P));  // per launch, as above
         CUDA_OK(cudaLaunchKernel(gather_stage_fn<T>(P), dim3(grid), dim3(P.gather_nt), args,
                                  static_cast<size_t>(gather_stage_smem<T>(P)), st));
         return;
@@ -1810,8 +1843,7 @@ void launch_windowed(const Plan& P, dev::WinArgs<T> A, int ctas, cudaStream_t st
     if (P.value_symmetric) A.au = A.al;
     auto fn = windowed_fn<T>(P.win_lanes, P.tile_rows, P.win_ring);
     // per-plan shared-memory size: the attribute is per function, so set it per launch
-    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(P.win_smem)));
+    set_smem_limit(reinterpret_cast<const void*>(fn), static_cast<int>(P.win_smem));
     fn<<<ctas, 32 + P.tile_rows * P.win_lanes, P.win_smem, st>>>(A);
 }
 
@@ -1923,14 +1955,48 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
     CUDA_OK(cudaGetLastError());
 }
 
+// Products that touch plan-owned scratch (local-buffers band buffers, the timing
+// events, the colored plan's class-order vectors) on a caller stream other than
+// the plan's own are ordered both ways against the plan's stream, so host
+// applies / time_products (plan stream) and apply_device (caller stream) on one
+// plan never overlap on that scratch. Skipped while the caller's stream is
+// capturing a graph (the capture orders itself).
+struct StreamJoin {
+    Plan& P;
+    cudaStream_t st;
+    bool on = false;
+    StreamJoin(Plan& p, cudaStream_t s, bool uses_scratch) : P(p), st(s) {
+        if (!uses_scratch || st == P.stream) return;
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CUDA_OK(cudaStreamIsCapturing(st, &cs));
+        if (cs != cudaStreamCaptureStatusNone) return;
+        for (auto& e : P.ev_join)
+            if (!e) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_OK(cudaEventRecord(P.ev_join[0], P.stream));
+        CUDA_OK(cudaStreamWaitEvent(st, P.ev_join[0], 0));
+        on = true;
+    }
+    void done() {
+        if (!on) return;
+        CUDA_OK(cudaEventRecord(P.ev_join[1], st));
+        CUDA_OK(cudaStreamWaitEvent(P.stream, P.ev_join[1], 0));
+    }
+};
+
+bool uses_plan_scratch(const Plan& P) {
+    return P.timing || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS || P.exec_kind == CSRC_KIND_COLORFUL;
+}
+
 void apply_device(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, int part = -1) {
     if (tr && P.is_csr) throw Error("spmv_csr: CSR plans have no transpose product");
     if (P.nrows == 0) return;
     CUDA_OK(cudaSetDevice(P.device));
+    StreamJoin join(P, st, uses_plan_scratch(P));
     if (P.dtype == CSRC_DTYPE_F64)
         apply_typed<double>(P, dx, dy, st, tr, part);
     else
         apply_typed<float>(P, dx, dy, st, tr, part);
+    join.done();
 }
 
 // Host product with the copies overlapped (gather plans): x goes up in row
@@ -2548,10 +2614,12 @@ int csrc_gpu_time_products_host(csrc_gpu_plan_t plan, const double* x_host, int6
         if (!P.dx.p) P.dx.alloc(nx * P.vsize());
         if (!P.dy.p) P.dy.alloc(static_cast<size_t>(P.n_global) * P.vsize());
         if (P.dtype == CSRC_DTYPE_F64) {
-            CUDA_OK(cudaMemcpy(P.dx.p, x_host, nx * 8, cudaMemcpyHostToDevice));
+            CUDA_OK(cudaMemcpyAsync(P.dx.p, x_host, nx * 8, cudaMemcpyHostToDevice, P.stream));
+            CUDA_OK(cudaStreamSynchronize(P.stream));
         } else {
             std::vector<float> xf(x_host, x_host + nx);
-            CUDA_OK(cudaMemcpy(P.dx.p, xf.data(), nx * 4, cudaMemcpyHostToDevice));
+            CUDA_OK(cudaMemcpyAsync(P.dx.p, xf.data(), nx * 4, cudaMemcpyHostToDevice, P.stream));
+            CUDA_OK(cudaStreamSynchronize(P.stream));
         }
         if (csrc_gpu_time_products(plan, P.dx.p, P.dy.p, reps, flush_bytes, ms_out, kernel_ms_out) != 0)
             throw Error(csrc_gpu_last_error());

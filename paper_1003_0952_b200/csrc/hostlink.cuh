@@ -85,7 +85,12 @@ public:
 
     void h2d(void* dev, const void* host, size_t bytes) {
         if (bytes <= kSmall) {
-            if (bytes) HL_CUDA(cudaMemcpy(dev, host, bytes, cudaMemcpyHostToDevice));
+            // on st_ + a sync: a pageable cudaMemcpy may return before its DMA lands, and
+            // kernels on non-blocking streams are not ordered after the legacy stream
+            if (bytes) {
+                HL_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, st_));
+                HL_CUDA(cudaStreamSynchronize(st_));
+            }
             return;
         }
         ready();
@@ -103,7 +108,10 @@ public:
 
     void d2h(void* host, const void* dev, size_t bytes) {
         if (bytes <= kSmall) {
-            if (bytes) HL_CUDA(cudaMemcpy(host, dev, bytes, cudaMemcpyDeviceToHost));
+            if (bytes) {
+                HL_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, st_));
+                HL_CUDA(cudaStreamSynchronize(st_));
+            }
             return;
         }
         ready();

@@ -1,4 +1,4 @@
-"""The product's direct CSRC fixture assembly (csrc/fixtures.cpp) equals the
+"""The product's direct CSRC fixture assembly (fixtures/csrc_fixtures.cpp) equals the
 reference pipeline build_csr -> csr_to_csrc applied to the restated mesh
 entries: golden vectors (reference output) for small meshes, live reference
 (oracle/_ref) for C1 and C2 at full size when it is present."""
@@ -73,3 +73,15 @@ def test_oracle_spmv_on_config_c1():
     a, x, _ = P.config_matrix("c1")
     y = Oracle().spmv_csrc(a, x)
     assert y.shape == (a.n,) and np.isfinite(y).all()
+
+
+@pytest.mark.parametrize("mesh,dims", [(0, (9, 7, 1)), (1, (6, 5, 4)), (2, (4, 3, 5)), (3, (7, 6, 5))])
+def test_standalone_fixture_library_equals_the_product_generator(mesh, dims):
+    """oracle/_build/libcsrc_fixtures.so (the reference arm's input generator)
+    and the product library build the same matrices from the same source."""
+    from oracle.oracle import fixture
+    a, x, _ = P.generate_fixture(P.Mesh(mesh), *dims, 5, 30.0)
+    b, xb = fixture(mesh, *dims, 5, 30.0)
+    for f in ("ad", "ia", "ja", "al", "au"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert np.array_equal(x, xb)

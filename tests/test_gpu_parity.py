@@ -573,6 +573,80 @@ def test_gather_kernel_shapes(shape, monkeypatch):
         assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.gather)), FAM[p + "y"]) <= TOL64
 
 
+GATHER_SHAPES_F32 = [
+    {},                                   # fp32 default: one row per thread, 6-block bound
+    {"CSRC_GPU_GMINB": "1"},              # the unbounded one-row-per-thread form
+    {"CSRC_GPU_GLANES": "2"},
+    {"CSRC_GPU_GLANES": "3"},             # not instantiated: falls back to the default lanes
+    {"CSRC_GPU_GLANES": "1", "CSRC_GPU_GPATTERN": "0"},
+    {"CSRC_GPU_GSELL": "1"},
+]
+
+
+@pytest.mark.parametrize("shape", range(len(GATHER_SHAPES_F32)))
+def test_gather_kernel_shapes_fp32(shape, monkeypatch):
+    """fp32 gather shapes (the fp32-only defaults included) against the fp64
+    oracle on fp32-rounded inputs."""
+    for k, v in GATHER_SHAPES_F32[shape].items():
+        monkeypatch.setenv(k, v)
+    for idx in (0, 3, 5):
+        p = f"g{idx}_"
+        a = MESH.matrix(p)
+        x32 = MESH[p + "x"].astype(np.float32).astype(np.float64)
+        ref = O.spmv_csrc(round32(a), x32)
+        y = run(a, x32, P.Strategy(K.gather, dtype=P.DType.f32))
+        assert rel_l2(y, ref) <= TOL32
+
+
+@pytest.mark.parametrize("dtype", [P.DType.f64, P.DType.f32])
+def test_smaller_plan_does_not_break_a_live_larger_plan(dtype):
+    """the dynamic shared-memory limit is an attribute of the
+    kernel function that plans of one shape share. A large plan stays alive, a
+    small plan of the same shape is created and run, then the large plan runs
+    again and must still launch and match."""
+    big, xb, _ = P.config_matrix("c2")
+    small = MESH.matrix("g0_")
+    ref_big = O.spmv_csrc(big, xb) if dtype == P.DType.f64 else O.spmv_csrc(
+        round32(big), xb.astype(np.float32).astype(np.float64))
+    xb_in = xb if dtype == P.DType.f64 else xb.astype(np.float32).astype(np.float64)
+    tol = TOL64 if dtype == P.DType.f64 else TOL32
+    for kind in (K.gather, K.windowed, K.local_buffers):
+        ex_big = P.GpuSpmv(big, P.Strategy(kind, p=4, dtype=dtype))
+        assert rel_l2(ex_big.apply(xb_in), ref_big) <= tol
+        ex_small = P.GpuSpmv(small, P.Strategy(kind, p=4, dtype=dtype))
+        ex_small.apply(MESH["g0_x"])
+        assert rel_l2(ex_big.apply(xb_in), ref_big) <= tol, kind.name
+        ex_small.close()
+        ex_big.close()
+
+
+@pytest.mark.parametrize("kind", [K.local_buffers, K.colorful, K.gather])
+def test_mixing_plan_and_caller_streams(kind):
+    """host apply() / time_products() run on the plan's own
+    stream, apply_device on the caller's; a plan's scratch (band buffers, class-
+    order vectors, timing events) is ordered across both."""
+    import torch
+    a, x, _ = P.config_matrix("c2")
+    ref = O.spmv_csrc(a, x)
+    ex = P.GpuSpmv(a, P.Strategy(kind, P.AccumMethod.interval, p=4))
+    ex.set_timing(True)
+    xd = torch.from_numpy(x).cuda()
+    side = torch.cuda.Stream()
+    outs = []
+    for i in range(4):
+        with torch.cuda.stream(side):
+            yd = torch.full_like(xd, float("nan"))
+            ex.apply_device(xd, yd)
+            outs.append(yd)
+        yh = ex.apply(x)  # plan stream, same scratch
+        assert rel_l2(yh, ref) <= TOL64
+        ex.time_products(xd, torch.empty_like(xd), 2)
+    torch.cuda.synchronize()
+    for yd in outs:
+        assert rel_l2(yd.cpu().numpy(), ref) <= TOL64
+    ex.close()
+
+
 @pytest.mark.parametrize("lanes", ["1", "2", "4"])
 def test_windowed_shared_memory_rings(lanes, monkeypatch):
     """The windowed kernel's optional shared-memory rings (CSRC_GPU_WIN_RINGS=1:
