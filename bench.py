@@ -132,7 +132,7 @@ def cpu_reference_suite(a, x, seconds, ref_threads=None):
     p = ref_threads or max(1, hc["physical"])
     methods = {}
     if Ref.available():
-        R = Ref()
+        R = Ref(fast=True)  # the host's ISA-level build (timed baseline)
         per = seconds / len(REF_METHODS)
         for name, kind, accum in REF_METHODS:
             h = R.exec_create(a, kind, accum, 1 if kind == 0 else p)
@@ -196,7 +196,7 @@ def run_reference_arm(args, world, rank):
     per_step = []
     suite = None
     if Ref.available():
-        R = Ref()
+        R = Ref(fast=True)  # the host's ISA-level build (timed baseline)
         # pick the reference's fastest method on this host (one product each), then time it
         probe = {}
         for name, kind, accum in REF_METHODS:

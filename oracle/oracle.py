@@ -59,7 +59,11 @@ def _ref_so() -> str:
     return os.path.join(HERE, "_ref", "libcsrc_ref.so")
 
 
-REF_SO = _ref_so()
+# The checker is the x86-64-v2 build: no FMA contraction, so its arithmetic is the
+# plain-C oracle's bit for bit (tests/test_oracle.py). The ISA-level builds are the
+# timed CPU baseline only (bench.py); with FMA their y differs in the last bits.
+REF_SO = os.path.join(HERE, "_ref", "libcsrc_ref.so")
+REF_SO_FAST = _ref_so()
 
 
 def host_cores() -> dict:
@@ -264,11 +268,12 @@ class Oracle:
 class Ref:
     """ctypes wrapper of the reference itself (oracle/_ref/libcsrc_ref.so)."""
 
-    def __init__(self):
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(REF_SO)
-        self.so = REF_SO
-        self.lib = C.CDLL(REF_SO)
+    def __init__(self, fast=False):
+        so = REF_SO_FAST if fast else REF_SO
+        if not os.path.exists(so):
+            raise FileNotFoundError(so)
+        self.so = so
+        self.lib = C.CDLL(so)
         L = self.lib
         L.ref_last_error.restype = C.c_char_p
         L.ref_trip_size.restype = C.c_int64

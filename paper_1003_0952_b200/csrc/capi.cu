@@ -11,6 +11,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <numeric>
+#include <tuple>
 #include <map>
 #include <mutex>
 #include <memory>
@@ -24,6 +26,7 @@
 #include "hostlink.cuh"
 #include "internal.hpp"
 #include "kernels.cuh"
+#include "colored.cuh"
 #include "plan_device.cuh"
 
 using namespace csrcgpu;
@@ -210,15 +213,24 @@ struct csrc_gpu_plan_s {
     cudaEvent_t ev_in = nullptr;
     std::vector<cudaEvent_t> ev_x, ev_y;
 
-    // local buffers
+    // local buffers: per-band spill buffers below each band's first row (kernels.cuh)
     DevBuf buf, boff, blo, bhi, bstart, iv_begin, iv_end, cptr, contrib;
+    DevBuf tile_band, band_rs, spill_shift;  // windowed schedule -> band; band first rows; spill offsets
     int n_iv = 0;
+    int lb_bands = 0;  // private buffers (the reference's p)
     count_t buf_total = 0;
 
     // colorful (class-major copy)
     int n_colors = 0;
     std::vector<count_t> class_ptr;
     DevBuf rid, cia, cja, cal, cau, cad;
+    // colorful wavefront (colored.cuh): block-major / class-major renumbering, SELL-32
+    // slices, (class, block) tasks dispatched by ticket; xp / yp scratch vectors
+    bool cw = false;
+    int cw_blocks = 0, cw_radius = 1, cw_tasks = 0, cw_tickets = 0, cw_grid = 0, cw_u = 8, cw_nt = 128;
+    int cw_pf = 1;
+    int64_t cw_rows = 0, cw_block_rows = 0;
+    DevBuf cw_tk, cw_nch, cw_ctr, cw_xp, cw_yp;
 
     // host-path scratch
     DevBuf dx, dy, dxd, dyd, flushbuf;
@@ -409,7 +421,8 @@ std::vector<int32_t> make_tiles(const Plan& P, const MatView& a, const std::vect
 // round-robin over `ctas` CTAs. Uploaded as per-tile descriptors.
 void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_t>& tiles,
                    const std::vector<int32_t>& band_first, int run_len, int ctas,
-                   DevBuf& d_desc, DevBuf& d_cta_ptr) {
+                   DevBuf& d_desc, DevBuf& d_cta_ptr, DevBuf* d_tile_band = nullptr,
+                   const std::vector<index_t>* band_starts = nullptr) {
     const int n_tiles = static_cast<int>(tiles.size()) - 1;
     std::vector<std::vector<std::pair<int32_t, int32_t>>> per(static_cast<size_t>(std::max(ctas, 1)));
     std::vector<int> runs_of(per.size(), 0);
@@ -445,6 +458,15 @@ void make_schedule(const MatView& a, index_t row_begin, const std::vector<int32_
     }
     upload(d_desc, desc.data(), desc.size());
     upload(d_cta_ptr, ptr.data(), ptr.size());
+    if (d_tile_band && band_starts) {  // band of every scheduled tile (tiles never straddle bands)
+        std::vector<int32_t> tb(desc.size());
+        for (size_t i = 0; i < desc.size(); ++i) {
+            const index_t r0 = desc[i].r0 & dev::kRowMask;
+            tb[i] = static_cast<int32_t>(std::upper_bound(band_starts->begin(), band_starts->end(), r0) -
+                                         band_starts->begin()) - 1;
+        }
+        upload(*d_tile_band, tb.data(), tb.size());
+    }
 }
 
 template <class T>
@@ -536,10 +558,13 @@ int pick_win_lanes(count_t k, index_t n, bool rings) {
 
 
 
+// lb_bands (local buffers): the wavefront schedule of the plain windowed kernel,
+// its tiles split at these band starts, plus the tile -> band map (rings off:
+// the spill routing lives in the ring-free path).
 template <class T>
 void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
-                    int requested_bands, bool banded) {
-    P.win_ring = win_rings();
+                    int requested_bands, bool banded, const std::vector<index_t>* lb_bands = nullptr) {
+    P.win_ring = lb_bands ? false : win_rings();
     P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows, P.win_ring));
     if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4)
         throw Error("windowed lanes per row must be 1, 2 or 4");
@@ -595,12 +620,13 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
         P.bands = static_cast<int>(bs.size()) - 1;
         make_schedule(a, P.row_begin, tiles, band_first, 0, P.bands, P.sched, P.cta_ptr);
     } else {
-        bs = {0, P.nrows};
+        bs = lb_bands ? *lb_bands : std::vector<index_t>{0, P.nrows};
         std::vector<int32_t> tiles = make_tiles(P, a, bs, band_first);
         P.n_tiles = static_cast<int>(tiles.size()) - 1;
         const int n_runs = (P.n_tiles + run_len - 1) / run_len;
         P.bands = std::max(1, std::min(resident, n_runs));
-        make_schedule(a, P.row_begin, tiles, band_first, run_len, P.bands, P.sched, P.cta_ptr);
+        make_schedule(a, P.row_begin, tiles, band_first, run_len, P.bands, P.sched, P.cta_ptr,
+                      lb_bands ? &P.tile_band : nullptr, lb_bands);
     }
     P.band_rows = bs;
     if (P.row_begin > 0 || P.row_end < P.n_global) {
@@ -635,7 +661,10 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.out = static_cast<T*>(out);
     A.tiles = P.sched.as<dev::TileDesc>();
     A.cta_ptr = P.cta_ptr.as<int32_t>();
-    A.band_shift = nullptr;
+    A.tile_band = nullptr;  // local buffers set the spill routing (apply_typed)
+    A.band_rs = nullptr;
+    A.spill_shift = nullptr;
+    A.spill = nullptr;
     A.shift = -static_cast<int64_t>(P.lo);
     A.xshift = -static_cast<int64_t>(P.lo);
     A.row_begin = P.row_begin;
@@ -655,23 +684,37 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
 template <class T>
 void setup_buffers(Plan& P, const MatView& a, const std::vector<index_t>* explicit_bs,
                    int requested_bands) {
-    setup_windowed<T>(P, a, explicit_bs, requested_bands, true);
-    const std::vector<index_t>& bs = P.band_rows;  // full plans: local == global rows
+    // p private buffers as in the reference (parallel.hpp:240-255): the caller's
+    // LocalBuffersPlan partition, else partition_by_nnz(a, p) with p = the
+    // strategy's thread count (or the device band override)
+    std::vector<index_t> bs;
+    if (explicit_bs) {
+        bs = *explicit_bs;
+    } else {
+        const int p = requested_bands > 0 ? requested_bands : std::max(1, P.p_ref);
+        bs = partition_by_nnz(a, std::min<int>(p, std::max<index_t>(a.n, 1))).block_start;
+    }
+    const int nb = static_cast<int>(bs.size()) - 1;
+    setup_windowed<T>(P, a, nullptr, 0, false, &bs);
+    P.band_rows = bs;
+    P.lb_bands = nb;
     std::vector<index_t> lo, hi;
     effective_ranges(a, bs, lo, hi);
-    std::vector<int64_t> off(P.bands + 1, 0), shift(P.bands);
-    for (int b = 0; b < P.bands; ++b) {
-        off[b + 1] = off[b] + (hi[b] - lo[b] + 1);
+    // spill buffer of band b: [lo_b, rs_b) (empty when nothing reaches below the band)
+    std::vector<int64_t> off(nb + 1, 0), shift(nb);
+    for (int b = 0; b < nb; ++b) {
+        const int64_t len = std::max<int64_t>(0, static_cast<int64_t>(bs[b]) - lo[b]);
+        off[b + 1] = off[b] + (bs[b + 1] > bs[b] ? len : 0);
         shift[b] = off[b] - lo[b];
     }
-    P.buf_total = off[P.bands];
+    P.buf_total = off[nb];
     IntervalPlan ip = build_interval_plan(lo, hi);
     P.n_iv = static_cast<int>(ip.iv_begin.size());
-    P.buf.alloc(static_cast<size_t>(P.buf_total) * sizeof(T));
+    P.buf.alloc(static_cast<size_t>(std::max<int64_t>(P.buf_total, 1)) * sizeof(T));
     upload(P.boff, off.data(), off.size());
-    upload(P.band_shift, shift.data(), shift.size());
+    upload(P.spill_shift, shift.data(), shift.size());
     upload(P.blo, lo.data(), lo.size());
-    upload(P.bhi, hi.data(), hi.size());
+    upload(P.band_rs, bs.data(), bs.size());
     upload(P.bstart, bs.data(), bs.size());
     upload(P.iv_begin, ip.iv_begin.data(), ip.iv_begin.size());
     upload(P.iv_end, ip.iv_end.data(), ip.iv_end.size());
@@ -682,25 +725,212 @@ void setup_buffers(Plan& P, const MatView& a, const std::vector<index_t>* explic
 template <class T>
 dev::BufArgs<T> buf_args(const Plan& P) {
     dev::BufArgs<T> B{};
-    B.buf = P.buf.as<T>();
-    B.boff = P.boff.as<int64_t>();
+    B.spill = P.buf.as<T>();
+    B.soff = P.boff.as<int64_t>();
     B.blo = P.blo.as<int32_t>();
-    B.bhi = P.bhi.as<int32_t>();
     B.bstart = P.bstart.as<int32_t>();
     B.iv_begin = P.iv_begin.as<int32_t>();
     B.iv_end = P.iv_end.as<int32_t>();
     B.cptr = P.cptr.as<int32_t>();
     B.contrib = P.contrib.as<int32_t>();
     B.n_iv = P.n_iv;
-    B.p = P.bands;
+    B.p = P.lb_bands;
     B.total = P.buf_total;
     return B;
 }
 
 // ------------------------------------------------------------- colorful
+// Wavefront form (colored.cuh, the default): rows grouped in blocks of
+// B >= bandwidth natural rows, renumbered block-major / class-major / ascending
+// with every (block, class) task 32-aligned; pairs in SELL-32 slices with
+// renumbered columns; tasks (e, b) -- e = 0 permute x in, 1..C the classes,
+// C + 1 permute y out -- cut into 128-row chunks (copy tasks: 1024 positions)
+// and dispatched in the topological order (floor((b + R e) / S), e, b).
+// instantiated shapes: (rows per chunk NT, entries in flight U, min CTAs per SM)
+template <class T, int NT>
+const void* colored_wave_fn_nt(int u) {
+    switch (u) {
+        case 16: return reinterpret_cast<const void*>(&dev::k_colored_wave<T, NT, 16, 512 / NT>);
+        case 4: return reinterpret_cast<const void*>(&dev::k_colored_wave<T, NT, 4, 1024 / NT>);
+        default: return reinterpret_cast<const void*>(&dev::k_colored_wave<T, NT, 8, 768 / NT>);
+    }
+}
+template <class T>
+const void* colored_wave_fn(const Plan& P) {
+    return P.cw_nt == 256 ? colored_wave_fn_nt<T, 256>(P.cw_u) : colored_wave_fn_nt<T, 128>(P.cw_u);
+}
+
+template <class T>
+void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& color, int C) {
+    const index_t n = a.n;
+    count_t bw = 0;
+    for (index_t i = 0; i < n; ++i)
+        if (a.ia[i + 1] > a.ia[i]) bw = std::max<count_t>(bw, i - a.ja[a.ia[i]]);
+    {
+        const int u = env_int("CSRC_GPU_CW_U", 8);
+        P.cw_u = (u == 4 || u == 16) ? u : 8;
+        P.cw_nt = env_int("CSRC_GPU_CW_NT", 128) == 256 ? 256 : 128;
+        P.cw_pf = env_int("CSRC_GPU_CW_PF", 1);
+    }
+    // blocks of B rows, R = ceil(bw / B): rows more than R blocks apart never write the
+    // same y position (row i writes only on [i - bw, i])
+    const int r_target = std::max(1, env_int("CSRC_GPU_CW_R", 4));
+    const int64_t min_rows = env_int("CSRC_GPU_CW_MINB", 32) * static_cast<int64_t>(C);
+    int64_t B = std::max<int64_t>({(bw + r_target - 1) / r_target, min_rows, 256});
+    B = std::min<int64_t>(B, std::max<index_t>(n, 1));
+    const int NB = static_cast<int>((n + B - 1) / B);
+    const int R = static_cast<int>(std::max<int64_t>(1, (bw + B - 1) / B));
+    P.cw_block_rows = B;
+    P.cw_blocks = NB;
+    P.cw_radius = R;
+    // task row counts and 32-aligned starts, block-major then class
+    std::vector<int64_t> cnt(static_cast<size_t>(NB) * C, 0), start(static_cast<size_t>(NB) * C + 1, 0);
+    for (index_t i = 0; i < n; ++i) ++cnt[static_cast<size_t>(i / B) * C + color[i]];
+    int64_t acc = 0;
+    for (size_t t = 0; t < cnt.size(); ++t) {
+        start[t] = acc;
+        acc += (cnt[t] + 31) / 32 * 32;
+    }
+    start[cnt.size()] = acc;
+    const int64_t npad = acc;
+    if (npad >= (int64_t(1) << 31)) throw Error("colorful: too many rows for the class-major layout");
+    P.cw_rows = npad;
+    std::vector<int32_t> pos(n), rid(static_cast<size_t>(npad), -1);
+    {
+        std::vector<int64_t> next(start.begin(), start.end() - 1);
+        for (index_t i = 0; i < n; ++i) {
+            const int64_t r = next[static_cast<size_t>(i / B) * C + color[i]]++;
+            pos[i] = static_cast<int32_t>(r);
+            rid[r] = i;
+        }
+    }
+    // tasks -> chunks: class chunks are NT consecutive class-major rows of one task,
+    // stored SELL-NT: entry q of the chunk's row t at ebase + q NT + t, the chunk's
+    // width w = its longest row (ebase 4-aligned for the bulk L2 prefetch)
+    const int NT = P.cw_nt;
+    const int NE = C + 2;
+    P.cw_tasks = NE * NB;
+    std::vector<int32_t> nch(P.cw_tasks, 0);
+    std::vector<std::vector<dev::CwTicket>> chunks(P.cw_tasks);
+    int64_t ne = 0;
+    for (int e = 0; e < NE; ++e)
+        for (int b = 0; b < NB; ++b) {
+            const int task = e * NB + b;
+            int64_t r0, r1, step;
+            if (e == 0 || e == NE - 1) {
+                r0 = start[static_cast<size_t>(b) * C];
+                r1 = start[static_cast<size_t>(b + 1) * C];
+                step = 1024;
+            } else {
+                r0 = start[static_cast<size_t>(b) * C + (e - 1)];
+                r1 = r0 + cnt[static_cast<size_t>(b) * C + (e - 1)];
+                step = NT;
+            }
+            for (int64_t q = r0; q < r1; q += step) {
+                dev::CwTicket t{};
+                t.task = task;
+                t.r0 = static_cast<int32_t>(q);
+                t.r1 = static_cast<int32_t>(std::min(r1, q + step));
+                t.e = e;
+                if (e >= 1 && e <= C) {
+                    int32_t w = 0;
+                    for (int64_t r = q; r < t.r1; ++r) w = std::max<int32_t>(w, a.ia[rid[r] + 1] - a.ia[rid[r]]);
+                    t.w = w;
+                    t.ebase = ne;
+                    ne += (static_cast<int64_t>(w) * NT + 3) / 4 * 4;
+                }
+                chunks[task].push_back(t);
+            }
+            // an empty task (a class absent from the block) still gets one empty chunk: it
+            // waits for its own dependencies before it counts as done, which keeps the
+            // waits transitive ((e, b) done => every (e', b') it transitively depends on done)
+            if (chunks[task].empty()) {
+                dev::CwTicket t{};
+                t.task = task;
+                t.r0 = t.r1 = static_cast<int32_t>(r0);
+                t.e = e;
+                chunks[task].push_back(t);
+            }
+            nch[task] = static_cast<int32_t>(chunks[task].size());
+        }
+    HVec<int32_t> cja(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+    HVec<double> cal(static_cast<size_t>(std::max<int64_t>(ne, 4))), cau, cad(static_cast<size_t>(npad), 0.0);
+    if (!a.value_symmetric) cau = HVec<double>(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+    for (int64_t r = 0; r < npad; ++r) cad[r] = rid[r] >= 0 ? a.ad[rid[r]] : 0.0;
+    std::vector<const dev::CwTicket*> cls;
+    for (auto& v : chunks)
+        for (auto& t : v)
+            if (t.e >= 1 && t.e <= C && t.w > 0) cls.push_back(&t);
+    parallel_slices(static_cast<int64_t>(cls.size()), [&](int, int64_t c0, int64_t c1) {
+        for (int64_t k = c0; k < c1; ++k) {
+            const dev::CwTicket& t = *cls[k];
+            const int64_t padded = (static_cast<int64_t>(t.w) * NT + 3) / 4 * 4;
+            for (int64_t z = static_cast<int64_t>(t.w) * NT; z < padded; ++z) {  // alignment tail
+                cja[t.ebase + z] = t.r0;
+                cal[t.ebase + z] = 0.0;
+                if (!a.value_symmetric) cau[t.ebase + z] = 0.0;
+            }
+            for (int32_t l = 0; l < NT; ++l) {
+                const int64_t r = static_cast<int64_t>(t.r0) + l;
+                const int32_t i = r < t.r1 ? rid[r] : -1;
+                const int32_t len = i >= 0 ? a.ia[i + 1] - a.ia[i] : 0;
+                for (int32_t q = 0; q < t.w; ++q) {
+                    const int64_t e = t.ebase + static_cast<int64_t>(q) * NT + l;
+                    if (q < len) {
+                        const int64_t s = a.ia[i] + q;
+                        cja[e] = pos[a.ja[s]];
+                        cal[e] = a.al[s];
+                        if (!a.value_symmetric) cau[e] = a.au[s];
+                    } else {  // padding: own row, zero values (never gathered nor scattered)
+                        cja[e] = static_cast<int32_t>(r);
+                        cal[e] = 0.0;
+                        if (!a.value_symmetric) cau[e] = 0.0;
+                    }
+                }
+            }
+        }
+    }, 64);
+    // dispatch along diagonals b + D e (D > R): class e trails class e-1 by D blocks, so
+    // (e, b)'s dependencies (e-1, b-R .. b+R) lie D - R diagonals earlier; all classes
+    // are in flight at once over a window of ~D (C + 2) blocks (x, y L2-resident)
+    const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", 4 * R));  // C5 1.72 ms vs 2.12 at 2R (profiles/r02_colored_wave_sweep.txt)
+    std::vector<int> order(P.cw_tasks);
+    std::iota(order.begin(), order.end(), 0);
+    auto key = [&](int t) {
+        const int e = t / NB, b = t % NB;
+        return std::make_tuple(b + D * e, e, b);
+    };
+    std::sort(order.begin(), order.end(), [&](int x, int y) { return key(x) < key(y); });
+    std::vector<dev::CwTicket> tk;
+    for (int t : order)
+        for (const dev::CwTicket& c : chunks[t]) tk.push_back(c);
+    P.cw_tickets = static_cast<int>(tk.size());
+    const size_t ne_up = static_cast<size_t>(std::max<int64_t>(ne, 4));
+    upload(P.rid, rid.data(), rid.size());
+    upload(P.cja, cja.data(), ne_up);
+    upload_values<T>(P.cal, cal.data(), ne_up);
+    if (!a.value_symmetric) upload_values<T>(P.cau, cau.data(), ne_up);
+    upload_values<T>(P.cad, cad.data(), static_cast<size_t>(npad));
+    upload(P.cw_tk, tk.data(), tk.size());
+    upload(P.cw_nch, nch.data(), nch.size());
+    P.cw_ctr.alloc(static_cast<size_t>(P.cw_tasks + 1) * 4);
+    P.cw_xp.alloc(static_cast<size_t>(npad) * sizeof(T));
+    P.cw_yp.alloc(static_cast<size_t>(npad) * sizeof(T));
+    const void* fn = colored_wave_fn<T>(P);
+    int occ = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P.cw_nt, 0));
+    const int per_sm = env_int("CSRC_GPU_CW_CTAS", std::max(occ, 1));
+    P.cw_grid = std::max(1, std::min(P.cw_tickets, num_sms(P.device) * std::min(per_sm, std::max(occ, 1))));
+    P.cw = true;
+}
+
 template <class T>
 void setup_colored(Plan& P, const MatView& a, const std::vector<int32_t>& color, int n_colors) {
     P.n_colors = n_colors;
+    if (env_int("CSRC_GPU_COLOR_WAVE", 1) != 0) {
+        setup_colored_wave<T>(P, a, color, n_colors);
+        return;
+    }
     const index_t n = a.n;
     P.class_ptr.assign(n_colors + 1, 0);
     for (index_t i = 0; i < n; ++i) ++P.class_ptr[color[i] + 1];
@@ -1671,7 +1901,7 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
                             std::to_string(v.row_b) + " both write y[" +
                             std::to_string(v.position) + "]");
             setup_colored<T>(P, a, color, nc);
-            P.launches = 1 + nc;
+            P.launches = P.cw ? 2 : 1 + nc;  // wave: counter memset + one persistent kernel
             break;
         }
         case CSRC_KIND_ATOMIC:
@@ -1824,7 +2054,38 @@ void launch_atomic(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
 }
 
 template <class T>
+void launch_colored_wave(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    dev::ColorWaveArgs<T> A{};
+    A.tickets = P.cw_tk.as<dev::CwTicket>();
+    A.nch = P.cw_nch.as<int32_t>();
+    A.ctr = P.cw_ctr.as<int32_t>();
+    A.n_tickets = P.cw_tickets;
+    A.n_blocks = P.cw_blocks;
+    A.n_e = P.n_colors + 2;
+    A.radius = P.cw_radius;
+    A.rid = P.rid.as<int32_t>();
+    A.ja = P.cja.as<int32_t>();
+    A.al = (tr ? P.cau : P.cal).template as<T>();
+    A.au = (tr ? P.cal : P.cau).template as<T>();
+    if (P.value_symmetric) A.au = A.al = P.cal.as<T>();
+    A.ad = P.cad.as<T>();
+    A.x = x;
+    A.y = y;
+    A.xp = P.cw_xp.as<T>();
+    A.yp = P.cw_yp.as<T>();
+    A.pf_mode = P.cw_pf;
+    // ticket counter + per-task completion counts start at zero every product
+    CUDA_OK(cudaMemsetAsync(P.cw_ctr.p, 0, static_cast<size_t>(P.cw_tasks + 1) * 4, st));
+    void* args[] = {&A};
+    CUDA_OK(cudaLaunchKernel(colored_wave_fn<T>(P), dim3(P.cw_grid), dim3(P.cw_nt), args, 0, st));
+}
+
+template <class T>
 void launch_colored(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    if (P.cw) {
+        launch_colored_wave<T>(P, tr, x, y, st);
+        return;
+    }
     const T* al = (tr ? P.cau : P.cal).template as<T>();
     const T* au = (tr ? P.cal : P.cau).template as<T>();
     if (P.value_symmetric) au = al = P.cal.as<T>();
@@ -1891,53 +2152,63 @@ void apply_typed(Plan& P, const void* dx, void* dy, cudaStream_t st, bool tr, in
             break;
         }
         case CSRC_KIND_COLORFUL: {
-            CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+            if (!P.cw) CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));  // the wave zeroes its own y
             rec(P, 1, st);
             launch_colored<T>(P, tr, x, y, st);
             rec(P, 2, st);
             break;
         }
         case CSRC_KIND_LOCAL_BUFFERS: {
+            // init: y (the owner parts of the buffers) and the spill buffers
             auto B = buf_args<T>(P);
             const int sms = num_sms(P.device);
-            switch (P.accum) {
-                case CSRC_ACCUM_ALL_IN_ONE:
-                    dev::k_init_flat<T><<<grid_for(P.device, P.buf_total, 256), 256, 0, st>>>(
-                        B.buf, P.buf_total);
-                    break;
-                case CSRC_ACCUM_PER_BUFFER:
-                case CSRC_ACCUM_EFFECTIVE: {
-                    dim3 g(std::max(1, sms * 4 / std::max(1, P.bands)), std::min(P.bands, 65535));
-                    dev::k_init_per_buffer<T><<<g, 256, 0, st>>>(B);
-                    break;
-                }
-                default: {
-                    dim3 g(std::max(1, sms * 4 / std::max(1, P.n_iv)),
-                           std::min(std::max(P.n_iv, 1), 65535));
-                    dev::k_init_interval<T><<<g, 256, 0, st>>>(B);
+            CUDA_OK(cudaMemsetAsync(y, 0, ybytes, st));
+            if (P.buf_total > 0) {
+                switch (P.accum) {
+                    case CSRC_ACCUM_ALL_IN_ONE:
+                        dev::k_init_flat<T><<<grid_for(P.device, P.buf_total, 256), 256, 0, st>>>(
+                            B.spill, P.buf_total);
+                        break;
+                    case CSRC_ACCUM_PER_BUFFER:
+                    case CSRC_ACCUM_EFFECTIVE: {
+                        dim3 g(std::max(1, sms * 4 / std::max(1, P.lb_bands)), std::min(P.lb_bands, 65535));
+                        dev::k_init_per_buffer<T><<<g, 256, 0, st>>>(B);
+                        break;
+                    }
+                    default: {
+                        dim3 g(std::max(1, sms * 4 / std::max(1, P.n_iv)), std::min(std::max(P.n_iv, 1), 65535));
+                        dev::k_init_interval<T><<<g, 256, 0, st>>>(B);
+                    }
                 }
             }
             rec(P, 1, st);
-            auto A = win_args<T>(P, dx, P.buf.p, tr);
-            A.band_shift = P.band_shift.as<int64_t>();
+            // compute: the wavefront windowed kernel, out-of-band scatters to the spills
+            auto A = win_args<T>(P, dx, dy, tr);
+            A.tile_band = P.tile_band.as<int32_t>();
+            A.band_rs = P.band_rs.as<int32_t>();
+            A.spill_shift = P.spill_shift.as<int64_t>();
+            A.spill = B.spill;
             launch_windowed<T>(P, A, P.bands, st);
             rec(P, 2, st);
+            // accumulate: y[q] += covering spills, ascending band id
             const int64_t shift = -static_cast<int64_t>(P.lo);
-            switch (P.accum) {
-                case CSRC_ACCUM_ALL_IN_ONE:
-                case CSRC_ACCUM_PER_BUFFER:
-                    dev::k_accum_sliced<T><<<grid_for(P.device, P.nrows, 256), 256, 0, st>>>(
-                        B, y, P.row_begin, P.row_end, shift);
-                    break;
-                case CSRC_ACCUM_EFFECTIVE: {
-                    dim3 g(std::max(1, sms * 4 / std::max(1, P.bands)), std::min(P.bands, 65535));
-                    dev::k_accum_effective<T><<<g, 256, 0, st>>>(B, y, shift);
-                    break;
-                }
-                default: {
-                    dim3 g(std::max(1, sms * 4 / std::max(1, P.n_iv)),
-                           std::min(std::max(P.n_iv, 1), 65535));
-                    dev::k_accum_interval<T><<<g, 256, 0, st>>>(B, y, shift);
+            if (P.buf_total > 0) {
+                switch (P.accum) {
+                    case CSRC_ACCUM_ALL_IN_ONE:
+                    case CSRC_ACCUM_PER_BUFFER: {
+                        dim3 g(4, std::min(std::max(P.lb_bands, 1) * 8, 65535));
+                        dev::k_accum_sliced<T><<<g, 256, 0, st>>>(B, y, P.row_begin, P.row_end, shift);
+                        break;
+                    }
+                    case CSRC_ACCUM_EFFECTIVE: {
+                        dim3 g(std::max(1, sms * 2 / std::max(1, P.lb_bands)), std::min(P.lb_bands, 65535));
+                        dev::k_accum_effective<T><<<g, 256, 0, st>>>(B, y, shift);
+                        break;
+                    }
+                    default: {
+                        dim3 g(std::max(1, sms * 2 / std::max(1, P.n_iv)), std::min(std::max(P.n_iv, 1), 65535));
+                        dev::k_accum_interval<T><<<g, 256, 0, st>>>(B, y, shift);
+                    }
                 }
             }
             break;
@@ -2347,8 +2618,8 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         info->k = P.k;
         info->kind = P.exec_kind;
         info->dtype = P.dtype;
-        info->bands = P.bands;
-        info->buffers_allocated = P.exec_kind == CSRC_KIND_LOCAL_BUFFERS ? P.bands : 0;
+        info->bands = P.exec_kind == CSRC_KIND_LOCAL_BUFFERS ? P.lb_bands : P.bands;
+        info->buffers_allocated = P.exec_kind == CSRC_KIND_LOCAL_BUFFERS ? P.lb_bands : 0;
         info->n_colors = P.n_colors;
         info->row_begin = P.row_begin;
         info->row_end = P.row_end;
@@ -2358,7 +2629,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
             csrc_model_bytes(P.nrows, band_nnz, P.value_symmetric ? 1 : 0, P.dtype);
         size_t dbytes = 0;
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
-                                &P.band_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
+                                &P.band_shift, &P.tile_band, &P.band_rs, &P.spill_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
                                 &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t, &P.xs_tab, &P.xs_clo, &P.xs_chi, &P.xs_cbase})
             if (d->p) dbytes += d->bytes;

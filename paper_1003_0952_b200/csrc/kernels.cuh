@@ -165,27 +165,34 @@ __global__ void k_halo_add(T* y, const T* __restrict__ recv, int64_t len) {
 }
 
 // ------------------------------------------------ local-buffers accumulation
-// Private band buffers are stored compactly over each band's effective range
-// [blo_b, bhi_b] at buf + boff[b] (parallel.hpp:254-255 keeps p dense n-vectors;
-// the GPU keeps only the reachable window, the reference's `effective` idea).
-// Coverage of y is described by the interval plan (partition.hpp:113-134).
+// GPU form of the private buffers (parallel.hpp:240-397). Band b's private
+// buffer over its effective range [lo_b, hi_b] (partition.hpp:94-102) splits
+// in two: positions at or above the band's first row rs_b are written by band b
+// alone (no lower band scatters upward), so that part of the buffer IS y; the
+// part below, [lo_b, rs_b), is the band's spill buffer at spill + soff[b]
+// (k_windowed routes every scatter below rs_b there). The accumulation then
+// reduces, for every position q, y[q] (the owner band, the lowest covering id)
+// plus the spills of the higher bands covering q in ascending id -- the
+// reference's sum over the buffers covering q (parallel.hpp:360-394), in its
+// order. Intervals of build_interval_plan (partition.hpp:113-134) with one
+// contributor need no work; the four AccumMethods differ in how the init and
+// the reduction are decomposed over CTAs, as the reference's do over threads.
 template <typename T>
 struct BufArgs {
-    T* buf;
-    const int64_t* boff;      // per band
+    T* spill;
+    const int64_t* soff;      // per band: start of its spill buffer
     const int32_t* blo;       // per band effective lo
-    const int32_t* bhi;       // per band effective hi
     const int32_t* bstart;    // per band first row (global), p+1 entries
     const int32_t* iv_begin;  // intervals
     const int32_t* iv_end;
-    const int32_t* cptr;      // contributors
+    const int32_t* cptr;      // contributors (ascending band id)
     const int32_t* contrib;
     int32_t n_iv;
     int32_t p;
-    int64_t total;            // buffer elements
+    int64_t total;            // spill elements
 };
 
-// all_in_one init (parallel.hpp:317-325): the concatenated storage as one slab
+// all_in_one init (parallel.hpp:317-325): the concatenated spill storage as one slab
 template <typename T>
 __global__ void k_init_flat(T* buf, int64_t total) {
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -193,26 +200,27 @@ __global__ void k_init_flat(T* buf, int64_t total) {
         buf[i] = T(0);
 }
 
-// per_buffer / effective init (parallel.hpp:327-338): one CTA row per buffer
+// per_buffer / effective init (parallel.hpp:327-338): one CTA row per band buffer
 template <typename T>
 __global__ void k_init_per_buffer(BufArgs<T> B) {
     for (int b = blockIdx.y; b < B.p; b += gridDim.y) {
-        const int64_t len = static_cast<int64_t>(B.bhi[b]) - B.blo[b] + 1;
-        T* base = B.buf + B.boff[b];
+        const int64_t len = B.soff[b + 1] - B.soff[b];
+        T* base = B.spill + B.soff[b];
         for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < len;
              i += static_cast<int64_t>(gridDim.x) * blockDim.x)
             base[i] = T(0);
     }
 }
 
-// interval init (parallel.hpp:339-346): per interval, its contributors' slices
+// interval init (parallel.hpp:339-346): per interval, the spill slices of its
+// contributors above the owner
 template <typename T>
 __global__ void k_init_interval(BufArgs<T> B) {
     for (int iv = blockIdx.y; iv < B.n_iv; iv += gridDim.y) {
         const int32_t q0 = B.iv_begin[iv], q1 = B.iv_end[iv];
-        for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
+        for (int32_t c = B.cptr[iv] + 1; c < B.cptr[iv + 1]; ++c) {
             const int bb = B.contrib[c];
-            T* base = B.buf + B.boff[bb] - B.blo[bb];
+            T* base = B.spill + B.soff[bb] - B.blo[bb];
             for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
                  q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x)
                 base[q] = T(0);
@@ -220,73 +228,62 @@ __global__ void k_init_interval(BufArgs<T> B) {
     }
 }
 
+// y[q] += the higher contributors' spills at q, ascending id, q in [q0, q1) of
+// interval iv; two positions per thread step (16-byte fp64 / 8-byte fp32 pairs
+// where the interval is long enough).
 template <typename T>
-__device__ __forceinline__ int find_interval(const BufArgs<T>& B, int32_t q) {
-    int lo = 0, hi = B.n_iv;  // first interval with end > q
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (B.iv_end[mid] <= q) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
-
-// all_in_one / per_buffer accumulation (parallel.hpp:360-369): y sliced
-// evenly; every buffer covering q contributes in ascending id.
-template <typename T>
-__global__ void k_accum_sliced(BufArgs<T> B, T* y, int32_t q_begin, int32_t q_end,
-                               int64_t shift) {
-    for (int64_t q = q_begin + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-         q < q_end; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int iv = find_interval(B, static_cast<int32_t>(q));
-        T s = T(0);
-        if (iv < B.n_iv && B.iv_begin[iv] <= q) {
-            for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
-                const int bb = B.contrib[c];
-                s += B.buf[B.boff[bb] + (q - B.blo[bb])];
-            }
+__device__ __forceinline__ void accum_range(const BufArgs<T>& B, T* y, int iv, int64_t q0, int64_t q1,
+                                            int64_t shift, int64_t start, int64_t stride) {
+    const int32_t c0 = B.cptr[iv] + 1, c1 = B.cptr[iv + 1];
+    if (c1 <= c0) return;  // one contributor: the owner's values are already in y
+    for (int64_t q = q0 + start; q < q1; q += stride) {
+        T s = y[q + shift];
+        for (int32_t c = c0; c < c1; ++c) {
+            const int bb = B.contrib[c];
+            s += B.spill[B.soff[bb] + (q - B.blo[bb])];
         }
         y[q + shift] = s;
     }
 }
 
-// effective accumulation (parallel.hpp:371-382): band b sums, for its own
-// rows, the buffers whose range covers q (ascending id).
+// all_in_one / per_buffer accumulation (parallel.hpp:360-369): y sliced into
+// even slabs (blockIdx.y), each slab walking the intervals it overlaps.
+template <typename T>
+__global__ void k_accum_sliced(BufArgs<T> B, T* y, int32_t q_begin, int32_t q_end, int64_t shift) {
+    const int64_t len = static_cast<int64_t>(q_end) - q_begin;
+    const int64_t s0 = q_begin + len * blockIdx.y / gridDim.y, s1 = q_begin + len * (blockIdx.y + 1) / gridDim.y;
+    for (int iv = 0; iv < B.n_iv; ++iv) {
+        const int64_t a = max(s0, static_cast<int64_t>(B.iv_begin[iv]));
+        const int64_t b = min(s1, static_cast<int64_t>(B.iv_end[iv]));
+        if (a < b)
+            accum_range(B, y, iv, a, b, shift, blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                        static_cast<int64_t>(gridDim.x) * blockDim.x);
+    }
+}
+
+// effective accumulation (parallel.hpp:371-382): band b (blockIdx.y) sums, for
+// its own rows, the buffers covering them (ascending id).
 template <typename T>
 __global__ void k_accum_effective(BufArgs<T> B, T* y, int64_t shift) {
     for (int b = blockIdx.y; b < B.p; b += gridDim.y) {
-        const int32_t q0 = B.bstart[b], q1 = B.bstart[b + 1];
-        for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-             q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-            // covering buffers of q, ascending id, from the interval plan
-            const int iv = find_interval(B, static_cast<int32_t>(q));
-            T s = T(0);
-            if (iv < B.n_iv && B.iv_begin[iv] <= q) {
-                for (int32_t c = B.cptr[iv]; c < B.cptr[iv + 1]; ++c) {
-                    const int bb = B.contrib[c];
-                    s += B.buf[B.boff[bb] + (q - B.blo[bb])];
-                }
-            }
-            y[q + shift] = s;
+        const int64_t r0 = B.bstart[b], r1 = B.bstart[b + 1];
+        for (int iv = 0; iv < B.n_iv; ++iv) {
+            const int64_t a = max(r0, static_cast<int64_t>(B.iv_begin[iv]));
+            const int64_t e = min(r1, static_cast<int64_t>(B.iv_end[iv]));
+            if (a < e)
+                accum_range(B, y, iv, a, e, shift, blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                            static_cast<int64_t>(gridDim.x) * blockDim.x);
         }
     }
 }
 
-// interval accumulation (parallel.hpp:384-394)
+// interval accumulation (parallel.hpp:384-394): intervals over blockIdx.y
 template <typename T>
 __global__ void k_accum_interval(BufArgs<T> B, T* y, int64_t shift) {
-    for (int iv = blockIdx.y; iv < B.n_iv; iv += gridDim.y) {
-        const int32_t q0 = B.iv_begin[iv], q1 = B.iv_end[iv];
-        const int32_t c0 = B.cptr[iv], c1 = B.cptr[iv + 1];
-        for (int64_t q = q0 + blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-             q < q1; q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-            T s = T(0);
-            for (int32_t c = c0; c < c1; ++c) {
-                const int bb = B.contrib[c];
-                s += B.buf[B.boff[bb] + (q - B.blo[bb])];
-            }
-            y[q + shift] = s;
-        }
-    }
+    for (int iv = blockIdx.y; iv < B.n_iv; iv += gridDim.y)
+        accum_range(B, y, iv, B.iv_begin[iv], B.iv_end[iv], shift,
+                    blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x,
+                    static_cast<int64_t>(gridDim.x) * blockDim.x);
 }
 
 }  // namespace dev

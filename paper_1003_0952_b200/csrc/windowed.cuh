@@ -68,7 +68,14 @@ struct WinArgs {
     T* out;                     // out[q + shift_b]
     const TileDesc* tiles;      // schedule: CTA b owns tiles[cta_ptr[b] .. cta_ptr[b+1])
     const int32_t* cta_ptr;
-    const int64_t* band_shift;  // per-CTA output shift (private buffers); null = shift
+    // local buffers (parallel.hpp:286-397, GPU form): each scheduled tile belongs to one
+    // band b; a scatter to q < band_rs[b] (below the band's first row) is band b's
+    // out-of-band contribution and goes to its spill buffer spill[q + spill_shift[b]];
+    // everything at or above band_rs[b] is band b's alone and goes to out. Null: all to out.
+    const int32_t* tile_band;
+    const int32_t* band_rs;
+    const int64_t* spill_shift;
+    T* spill;
     int64_t shift;
     int64_t xshift;
     int32_t row_begin;          // global id of local row 0
@@ -266,8 +273,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
     const int maskF = A.ring_far - 1;
     const bool far_on = A.far_lo <= A.far_hi;
     const int b = blockIdx.x;
-    const int64_t shift = A.band_shift ? A.band_shift[b] : A.shift;
-    T* __restrict__ out = A.out + shift;  // out indexed by global position
+    T* __restrict__ out = A.out + A.shift;  // out indexed by global position
     const bool sym = A.au == A.al;
     const int32_t s0 = A.cta_ptr[b];
     const int32_t t_count = A.cta_ptr[b + 1] - s0;
@@ -349,6 +355,13 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
         }
         mbar_wait(&full[s], (ti / S) & 1);
         const TileDesc dsc = descs[s];
+        int32_t rs = INT32_MIN;  // scatters below rs go to the tile's band spill buffer
+        T* sp = out;
+        if (!RINGS && A.tile_band) {
+            const int32_t bnd = A.tile_band[s0 + ti];
+            rs = A.band_rs[bnd];
+            sp = A.spill + A.spill_shift[bnd];
+        }
         const int32_t r0 = dsc.r0 & kRowMask;
         const int nr = dsc.r1 - r0;
         const int32_t g0 = A.row_begin + r0;
@@ -407,7 +420,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
                         yi = fma(lds_f(al_b + E * mm[u], T(0)), xv[u], yi);
                         val[u] = lds_f(au_b + E * mm[u], T(0)) * xi;
                         if (!RINGS) {
-                            red_add(out + j[u], val[u]);
+                            red_add((j[u] < rs ? sp : out) + j[u], val[u]);
                             continue;
                         }
                         const int32_t d = g - j[u];

@@ -134,6 +134,36 @@ def test_explicit_local_buffers_plan_2x2():
         ex.close()
 
 
+@pytest.mark.parametrize("p", [2, 3, 8, 148, 1000])
+def test_local_buffers_spill_form(p):
+    """The GPU private buffers: the part of band b's buffer at or above its
+    first row is y itself (no lower band writes there), the part below is a
+    spill buffer of effective_range lo .. first row (partition.hpp:94-102).
+    Every accumulation equals the oracle; the spill storage is the halo only,
+    not p dense n-vectors."""
+    a, x, _ = P.config_matrix("c2")
+    ref = O.spmv_csrc(a, x)
+    part = P.partition_by_nnz(a, p)
+    rng = P.effective_ranges(a, part)
+    halo = sum(max(0, part.begin(b) - r.lo) for b, r in enumerate(rng))
+    for acc in A:
+        ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, acc, p=p))
+        assert ex.buffers_allocated() == p
+        y = ex.apply(x)
+        assert rel_l2(y, ref) <= TOL64 and rel_inf(y, ref) <= TOL64, acc.name
+        ex.close()
+    # explicit uneven partition (LocalBuffersPlan given by the caller)
+    cut = sorted(set([0, 1, 7, a.n // 3, a.n // 3 + 5, a.n - 2, a.n]))
+    bs = P.RowPartition(len(cut) - 1, cut, [0] * (len(cut) - 1))
+    r2 = P.effective_ranges(a, bs)
+    plan = P.LocalBuffersPlan(bs, r2, P.build_interval_plan(r2))
+    for acc in A:
+        ex = P.GpuSpmv(a, P.Strategy(K.local_buffers, acc, p=bs.p), plan)
+        assert rel_l2(ex.apply(x), ref) <= TOL64, acc.name
+        ex.close()
+    assert halo < p * 70_000  # C2 bandwidth 4161: the spill is the halo only
+
+
 def test_mismatched_plans_throw():
     """test_parallel.cpp:159-165."""
     a = MESH.matrix("g0_")
@@ -354,29 +384,92 @@ def test_configs_full_size(cfg, kind):
     assert rel_l2(y, ref) <= TOL64 and rel_inf(y, ref) <= TOL64
 
 
-@pytest.mark.parametrize("kind", [K.windowed, K.gather])
+# every kernel kind x accumulation, the kinds the north star names included
+LARGE_KINDS = [
+    ("gather", P.Strategy(K.gather)),
+    ("windowed", P.Strategy(K.windowed)),
+    ("atomic", P.Strategy(K.atomic)),
+    ("colorful_nbh", P.Strategy(K.colorful, p=8)),
+    ("colorful_exact", P.Strategy(K.colorful, p=8, conflict_mode=P.ConflictMode.exact)),
+    ("lb_all_in_one", P.Strategy(K.local_buffers, A.all_in_one, p=8)),
+    ("lb_per_buffer", P.Strategy(K.local_buffers, A.per_buffer, p=8)),
+    ("lb_effective", P.Strategy(K.local_buffers, A.effective, p=8)),
+    ("lb_interval", P.Strategy(K.local_buffers, A.interval, p=8)),
+]
+_big = {}
+
+
+def big_config(cfg, f32=False):
+    """(a, x, y_ref) for a BASELINE config, one config resident at a time. The
+    oracle's full-size y is itself pinned to the reference's (sha256,
+    tests/test_config_pins.py); fp32: the fp64 oracle on fp32-rounded inputs."""
+    key = (cfg, f32)
+    if key not in _big:
+        _big.clear()
+        a, x, _ = P.config_matrix(cfg)
+        if f32:
+            x = x.astype(np.float32).astype(np.float64)
+            ref = O.spmv_csrc(round32(a), x)
+        else:
+            ref = O.spmv_csrc(a, x)
+        _big[key] = (a, x, ref)
+    return _big[key]
+
+
+@pytest.mark.parametrize("name,s", LARGE_KINDS, ids=[n for n, _ in LARGE_KINDS])
 @pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
-def test_large_configs(cfg, kind):
-    a, x, _ = P.config_matrix(cfg)
-    ref = O.spmv_csrc(a, x)
-    y = run(a, x, P.Strategy(kind))
-    assert rel_l2(y, ref) <= TOL64
-    # linearity, a size-independent property: A(x + 2 z) = A x + 2 A z
-    z = np.random.default_rng(1).uniform(-1, 1, a.n)
-    ex = P.GpuSpmv(a, P.Strategy(kind))
-    lhs = ex.apply(x + 2 * z)
-    rhs = ex.apply(x) + 2 * ex.apply(z)
-    assert rel_l2(lhs, rhs) <= 1e-13
-    ex.close()
+def test_large_configs(cfg, name, s):
+    a, x, ref = big_config(cfg)
+    ex = P.GpuSpmv(a, s)
+    try:
+        y = ex.apply(x)
+        assert rel_l2(y, ref) <= TOL64 and rel_inf(y, ref) <= TOL64, name
+        if name.startswith("colorful"):
+            assert ex.info().n_colors >= 2
+        if name in ("gather", "windowed", "colorful_nbh", "lb_interval"):
+            # linearity, a size-independent property: A(x + 2 z) = A x + 2 A z
+            z = np.random.default_rng(1).uniform(-1, 1, a.n)
+            lhs = ex.apply(x + 2 * z)
+            rhs = ex.apply(x) + 2 * ex.apply(z)
+            assert rel_l2(lhs, rhs) <= 1e-13
+        if name in ("gather", "colorful_nbh"):
+            assert np.array_equal(ex.apply(x), y)  # no atomics: bit-reproducible
+    finally:
+        ex.close()
 
 
-@pytest.mark.parametrize("kind", [K.windowed, K.gather])
-def test_c5_fp32(kind):
-    a, x, _ = P.config_matrix("c5")
-    x32 = x.astype(np.float32).astype(np.float64)
-    ref = O.spmv_csrc(round32(a), x32)
-    y = run(a, x32, P.Strategy(kind, dtype=P.DType.f32))
-    assert rel_l2(y, ref) <= TOL32
+@pytest.mark.parametrize("name,s", LARGE_KINDS, ids=[n for n, _ in LARGE_KINDS])
+def test_c5_fp32(name, s):
+    a, x32, ref = big_config("c5", f32=True)
+    s32 = P.Strategy(s.kind, s.accum, p=s.p, dtype=P.DType.f32, conflict_mode=s.conflict_mode)
+    y = run(a, x32, s32)
+    assert rel_l2(y, ref) <= TOL32, name
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_device_construction_matches_the_reference_at_scale(cfg):
+    """build_csr -> csr_to_csrc (csr.hpp:55-92, csrc_matrix.hpp:44-91) on the
+    device from the fixture's triplets in the golden shuffled order: the sha256
+    of every CSRC array equals the reference's own construction of the same
+    triplets (tests/golden/configs.json, made by oracle/_ref here)."""
+    import hashlib
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "configs.json")) as f:
+        g = json.load(f)
+    gc = g["construction"][cfg]
+    _big.clear()
+    a, _, _ = P.config_matrix(cfg)
+    n, _, r, c, v = P.csrc_to_triplets(a)
+    perm = np.random.default_rng(g["shuffle_seed"]).permutation(r.size)
+    r, c, v = r[perm], c[perm], v[perm]
+    del perm
+    assert r.size == gc["triplets"]
+    b = P.build_csrc((n, n, r, c, v))
+    del r, c, v
+    assert b.value_symmetric == gc["value_symmetric"]
+    for f in ("ad", "ia", "ja", "al", "au"):
+        assert hashlib.sha256(np.ascontiguousarray(getattr(b, f)).tobytes()).hexdigest() == gc[f], f
 
 
 @pytest.mark.parametrize("bands", [2, 3, 5])
