@@ -16,8 +16,8 @@
  *   RowPartition partition_by_nnz(const CsrcMatrix&, int p)    partition.hpp:55-90
  *   std::vector<EffectiveRange> effective_ranges(...)          partition.hpp:104-109
  *   IntervalPlan build_interval_plan(...)                      partition.hpp:113-134
- *   Coloring color_rows(build_conflict_graph(a, mode), order)  coloring.hpp:229-300
- *   ColoringValidity validate_coloring(const CsrcMatrix&, const Coloring&) coloring.hpp:311-334
+ *   Coloring color_rows(build_conflict_graph(a, mode), order)  coloring.hpp:93-164
+ *   ColoringValidity validate_coloring(const CsrcMatrix&, const Coloring&) coloring.hpp:175-198
  *   double working_set_kb(n, nnz_stored, value_symmetric)      working_set.hpp:17-25
  *
  * Every entry point below replaces one of those; the reference has no FFI of
@@ -160,7 +160,7 @@ int csrc_gpu_plan_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
 
 /* ParallelSpmv(a, s, ColorfulPlan) (parallel.hpp:163-166): explicit coloring.
  * The coloring is validated with the exact write-set check of
- * validate_coloring (coloring.hpp:311-334); an invalid one is rejected with
+ * validate_coloring (coloring.hpp:175-198); an invalid one is rejected with
  * "coloring violation: rows A and B both write y[Q]". */
 int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                                  const int32_t* color, int32_t n_colors,
@@ -198,6 +198,19 @@ int csrc_gpu_plan_create_rect(const csrc_host_matrix* a, const csrc_gpu_strategy
                               const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
                               const double* tail_values, csrc_gpu_plan_t* out);
 
+/* ParallelSpmv(const CsrcRectMatrix&, Strategy, ColorfulPlan | LocalBuffersPlan)
+ * (parallel.hpp:173-181): a rectangular plan with an explicit colouring
+ * (color[n], n_colors; block_start NULL) or band partition (block_start[bands+1];
+ * color NULL). */
+int csrc_gpu_plan_create_rect_plan(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t m_cols,
+                                   const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
+                                   const double* tail_values, const int32_t* color, int32_t n_colors,
+                                   const int32_t* block_start, int32_t bands, csrc_gpu_plan_t* out);
+
+/* ParallelSpmv::colorful_plan (parallel.hpp:226): the colouring a colorful plan
+ * runs (color[n] may be NULL to query *n_colors; 0 for other kinds). */
+int csrc_gpu_plan_get_coloring(csrc_gpu_plan_t plan, int32_t* color, int32_t* n_colors);
+
 void csrc_gpu_plan_destroy(csrc_gpu_plan_t plan);
 int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info);
 
@@ -207,6 +220,14 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info);
  * H2D of x, the product, D2H of y; returns after y is on the host.
  * ParallelSpmv::apply(x, y) (parallel.hpp:189-220) / spmv_csrc (kernels.hpp:25). */
 int csrc_gpu_spmv(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, double* y_host);
+
+/* One-shot spmv_csrc / spmv_csrc_transpose (kernels.hpp:25-65) of a host matrix,
+ * no plan: the CSRC arrays stream to the device as stored, row chunk by row chunk
+ * (pinned double-buffered staging, copies overlapped with the global-atomic kernel
+ * on the previous chunk); x, y host vectors of length n. For a single product the
+ * plan-free path wins: a plan's preprocessing costs seconds at C5. */
+int csrc_gpu_spmv_oneshot(const csrc_host_matrix* a, const double* x_host, int64_t x_len, double* y_host,
+                          int32_t transpose, int32_t device);
 
 /* spmv_csrc_transpose (kernels.hpp:47-65): al/au swapped, zero-copy. */
 int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len,
@@ -290,7 +311,7 @@ int csrc_interval_plan(int32_t p, const int32_t* lo, const int32_t* hi, int32_t*
                        int32_t* iv_end, int32_t* contrib_ptr, int32_t* contrib,
                        int32_t* boundaries);
 
-/* color_rows(build_conflict_graph(a, mode), order) (coloring.hpp:229-300):
+/* color_rows(build_conflict_graph(a, mode), order) (coloring.hpp:93-164):
  * color[n], *n_colors. CSR adjacency, no std::set; identical first-fit result. */
 int csrc_color_rows(const csrc_host_matrix* a, int32_t mode, int32_t order, int32_t* color,
                     int32_t* n_colors);
@@ -299,7 +320,7 @@ int csrc_color_rows(const csrc_host_matrix* a, int32_t mode, int32_t order, int3
 int csrc_conflict_edge_counts(const csrc_host_matrix* a, int32_t mode, int64_t* n_direct,
                               int64_t* n_indirect);
 
-/* validate_coloring (coloring.hpp:311-334): returns 0 and sets *valid; on a
+/* validate_coloring (coloring.hpp:175-198): returns 0 and sets *valid; on a
  * violation row_a, row_b, position describe the first violating pair. */
 int csrc_validate_coloring(const csrc_host_matrix* a, const int32_t* color, int32_t n_colors,
                            int32_t* valid, int32_t* row_a, int32_t* row_b, int32_t* position);
@@ -310,7 +331,7 @@ int csrc_colorful_slices(const csrc_host_matrix* a, const int32_t* color, int32_
                          int32_t p, int64_t* slices);
 
 /* working_set_kb (working_set.hpp:17-25) in bytes, and count_ops flops
- * (cost_model.hpp:67-89, Format::csrc / csrc_sym). */
+ * (cost_model.hpp:20-42, Format::csrc / csrc_sym). */
 int64_t csrc_model_bytes(int64_t n, int64_t nnz_stored, int32_t value_symmetric, int32_t dtype);
 int64_t csrc_model_flops(int64_t n, int64_t nnz_full);
 

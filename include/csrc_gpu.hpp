@@ -13,7 +13,8 @@
 // csrc::ColorfulPlan are accepted unchanged:
 //
 //     #include <csrc/csrc.hpp>          // reference
-//     #define CSRC_GPU_ERROR_TYPE csrc::Error   // optional: throw the reference's error type
+//     #define CSRC_GPU_REFERENCE_TYPES   // optional: the reference's own Error, PhaseTimings,
+//                                        // Strategy, LocalBuffersPlan, ColorfulPlan types in and out
 //     #include <csrc_gpu.hpp>
 //     csrc::Vector y = csrc::gpu::spmv_csrc(c, x);
 //     csrc::gpu::ParallelSpmv exec(c, csrc::Strategy{csrc::StrategyKind::local_buffers,
@@ -21,6 +22,7 @@
 //     csrc::Vector y2 = exec.apply(x);
 #pragma once
 
+#include <cstddef>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -31,6 +33,10 @@
 
 namespace csrc {
 namespace gpu {
+
+#if defined(CSRC_GPU_REFERENCE_TYPES) && !defined(CSRC_GPU_ERROR_TYPE)
+#define CSRC_GPU_ERROR_TYPE ::csrc::Error
+#endif
 
 #ifdef CSRC_GPU_ERROR_TYPE
 using Error = CSRC_GPU_ERROR_TYPE;
@@ -76,12 +82,53 @@ struct Strategy {
     }
 };
 
+#ifdef CSRC_GPU_REFERENCE_TYPES
+/// The reference's own csrc::PhaseTimings (parallel.hpp:26-30), so that
+/// `csrc::PhaseTimings t = exec.last_timings();` compiles unchanged.
+using PhaseTimings = ::csrc::PhaseTimings;
+using StrategyOut = ::csrc::Strategy;
+using BuffersPlanOut = ::csrc::LocalBuffersPlan;
+using ColorfulPlanOut = ::csrc::ColorfulPlan;
+#else
 /// csrc::PhaseTimings (parallel.hpp:26-30), seconds.
 struct PhaseTimings {
     double init_max = 0.0;
     double compute_max = 0.0;
     double accumulate_max = 0.0;
 };
+/// The plan a local-buffers executor runs (csrc::LocalBuffersPlan shape,
+/// parallel.hpp:40-52): partition, effective ranges, interval plan.
+struct BuffersPlanOut {
+    struct Partition {
+        int p = 1;
+        std::vector<int32_t> block_start;
+        std::vector<int64_t> block_nnz;
+    } partition;
+    struct Range {
+        int32_t lo = 0, hi = 0;
+    };
+    std::vector<Range> ranges;
+    struct Intervals {
+        struct Interval {
+            int32_t begin = 0, end = 0;
+            std::vector<int> contributors;
+        };
+        std::vector<int32_t> boundaries;
+        std::vector<Interval> intervals;
+    } intervals;
+};
+/// The colouring a colorful executor runs (csrc::ColorfulPlan shape,
+/// parallel.hpp:54-94).
+struct ColorfulPlanOut {
+    struct Coloring {
+        std::vector<int> color;
+        int n_colors = 0;
+        std::vector<std::vector<int32_t>> classes;
+    } coloring;
+    std::vector<std::vector<std::pair<std::size_t, std::size_t>>> class_slices;
+};
+using StrategyOut = Strategy;
+#endif
 
 /// Borrowed C view of any CsrcMatrix-shaped type (csrc_matrix.hpp:14-30).
 template <class M>
@@ -103,48 +150,199 @@ struct has_square : std::false_type {};
 template <class P>
 struct has_square<P, std::void_t<decltype(std::declval<P>().square)>> : std::true_type {};
 
-/// GPU counterpart of csrc::ParallelSpmv (parallel.hpp:151-446). Unlike the
-/// reference it copies the matrix (device-resident), so `a` may be freed.
+namespace detail {
+template <class P, class = void>
+struct has_coloring : std::false_type {};
+template <class P>
+struct has_coloring<P, std::void_t<decltype(std::declval<P>().coloring)>> : std::true_type {};
+
+template <class S>
+StrategyOut strategy_out(const S& s) {
+#ifdef CSRC_GPU_REFERENCE_TYPES
+    StrategyOut o;
+    o.kind = static_cast<decltype(o.kind)>(static_cast<int>(s.kind));
+    o.accum = static_cast<decltype(o.accum)>(static_cast<int>(s.accum));
+    o.p = s.p;
+    return o;
+#else
+    return Strategy(s);
+#endif
+}
+
+/// LocalBuffersPlan::build (parallel.hpp:45-51) through the product's plan
+/// functions (bit-exact with partition.hpp:55-134).
+inline BuffersPlanOut build_buffers_plan(const csrc_host_matrix& m, int p) {
+    BuffersPlanOut plan;
+    std::vector<int32_t> bs(static_cast<size_t>(p) + 1);
+    std::vector<int64_t> bn(static_cast<size_t>(p));
+    check(csrc_partition_by_nnz(&m, p, bs.data(), bn.data()));
+    plan.partition.p = p;
+    plan.partition.block_start.assign(bs.begin(), bs.end());
+    plan.partition.block_nnz.assign(bn.begin(), bn.end());
+    std::vector<int32_t> lo(static_cast<size_t>(p)), hi(static_cast<size_t>(p));
+    check(csrc_effective_ranges(&m, p, bs.data(), lo.data(), hi.data()));
+    plan.ranges.resize(static_cast<size_t>(p));
+    for (int t = 0; t < p; ++t) {
+        plan.ranges[t].lo = lo[t];
+        plan.ranges[t].hi = hi[t];
+    }
+    int32_t ni = 0, nc = 0, nb = 0;
+    check(csrc_interval_plan(p, lo.data(), hi.data(), &ni, &nc, &nb, nullptr, nullptr, nullptr, nullptr, nullptr));
+    std::vector<int32_t> ib(ni + 1), ie(ni + 1), cp(ni + 1), cc(nc + 1), bd(nb + 1);
+    check(csrc_interval_plan(p, lo.data(), hi.data(), &ni, &nc, &nb, ib.data(), ie.data(), cp.data(), cc.data(),
+                             bd.data()));
+    plan.intervals.boundaries.assign(bd.begin(), bd.begin() + nb);
+    plan.intervals.intervals.resize(static_cast<size_t>(ni));
+    for (int i = 0; i < ni; ++i) {
+        auto& iv = plan.intervals.intervals[i];
+        iv.begin = ib[i];
+        iv.end = ie[i];
+        iv.contributors.assign(cc.begin() + cp[i], cc.begin() + cp[i + 1]);
+    }
+    return plan;
+}
+
+/// ColorfulPlan (parallel.hpp:54-94) of the colouring a GPU plan runs, sliced
+/// for p workers (ColorfulPlan::slice, parallel.hpp:69-93).
+inline ColorfulPlanOut colorful_plan_of(csrc_gpu_plan_t plan, const csrc_host_matrix& m, int p) {
+    ColorfulPlanOut out;
+    int32_t nc = 0;
+    check(csrc_gpu_plan_get_coloring(plan, nullptr, &nc));
+    std::vector<int32_t> color(static_cast<size_t>(m.n));
+    check(csrc_gpu_plan_get_coloring(plan, color.data(), &nc));
+    out.coloring.color.assign(color.begin(), color.end());
+    out.coloring.n_colors = nc;
+    out.coloring.classes.assign(static_cast<size_t>(nc), {});
+    for (int32_t i = 0; i < m.n; ++i) out.coloring.classes[color[i]].push_back(i);
+    std::vector<int64_t> sl(static_cast<size_t>(std::max(nc, 1)) * p * 2);
+    check(csrc_colorful_slices(&m, color.data(), nc, p, sl.data()));
+    out.class_slices.assign(static_cast<size_t>(nc), std::vector<std::pair<std::size_t, std::size_t>>(p));
+    for (int c = 0; c < nc; ++c)
+        for (int t = 0; t < p; ++t)
+            out.class_slices[c][t] = {static_cast<std::size_t>(sl[(static_cast<size_t>(c) * p + t) * 2]),
+                                      static_cast<std::size_t>(sl[(static_cast<size_t>(c) * p + t) * 2 + 1])};
+    return out;
+}
+
+template <class Plan>
+BuffersPlanOut buffers_plan_copy(const Plan& plan) {
+    if constexpr (std::is_same<Plan, BuffersPlanOut>::value) {
+        return plan;
+    } else {
+        BuffersPlanOut o;
+        o.partition.p = plan.partition.p;
+        o.partition.block_start.assign(plan.partition.block_start.begin(), plan.partition.block_start.end());
+        o.partition.block_nnz.assign(plan.partition.block_nnz.begin(), plan.partition.block_nnz.end());
+        o.ranges.resize(plan.ranges.size());
+        for (size_t t = 0; t < plan.ranges.size(); ++t) {
+            o.ranges[t].lo = plan.ranges[t].lo;
+            o.ranges[t].hi = plan.ranges[t].hi;
+        }
+        o.intervals.boundaries.assign(plan.intervals.boundaries.begin(), plan.intervals.boundaries.end());
+        o.intervals.intervals.resize(plan.intervals.intervals.size());
+        for (size_t i = 0; i < plan.intervals.intervals.size(); ++i) {
+            o.intervals.intervals[i].begin = plan.intervals.intervals[i].begin;
+            o.intervals.intervals[i].end = plan.intervals.intervals[i].end;
+            o.intervals.intervals[i].contributors.assign(plan.intervals.intervals[i].contributors.begin(),
+                                                         plan.intervals.intervals[i].contributors.end());
+        }
+        return o;
+    }
+}
+
+template <class Plan>
+ColorfulPlanOut colorful_plan_copy(const Plan& plan) {
+    if constexpr (std::is_same<Plan, ColorfulPlanOut>::value) {
+        return plan;
+    } else {
+        ColorfulPlanOut o;
+        o.coloring.color.assign(plan.coloring.color.begin(), plan.coloring.color.end());
+        o.coloring.n_colors = plan.coloring.n_colors;
+        o.coloring.classes.resize(plan.coloring.classes.size());
+        for (size_t c = 0; c < plan.coloring.classes.size(); ++c)
+            o.coloring.classes[c].assign(plan.coloring.classes[c].begin(), plan.coloring.classes[c].end());
+        o.class_slices.resize(plan.class_slices.size());
+        for (size_t c = 0; c < plan.class_slices.size(); ++c)
+            for (const auto& pr : plan.class_slices[c])
+                o.class_slices[c].emplace_back(static_cast<std::size_t>(pr.first), static_cast<std::size_t>(pr.second));
+        return o;
+    }
+}
+}  // namespace detail
+
+/// GPU counterpart of csrc::ParallelSpmv (parallel.hpp:151-446): the same
+/// constructors (matrix or CsrcRectMatrix, Strategy, optional LocalBuffersPlan /
+/// ColorfulPlan, parallel.hpp:153-181), apply (:183-220), last_timings,
+/// buffers_allocated, strategy, buffers_plan, colorful_plan (:222-226). Unlike
+/// the reference it copies the matrix to the device, so `a` may be freed.
 class ParallelSpmv {
 public:
     template <class M, class S, std::enable_if_t<!has_square<M>::value, int> = 0>
-    ParallelSpmv(const M& a, const S& s) : n_(a.n) {
+    ParallelSpmv(const M& a, const S& s) : n_(a.n), x_len_(a.n), strategy_(detail::strategy_out(s)) {
         const csrc_host_matrix m = view(a);
         const csrc_gpu_strategy st = Strategy(s).c();
         check(csrc_gpu_plan_create(&m, &st, &plan_));
+        default_plans(m, st);
     }
 
-    /// ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181):
+    /// ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-171):
     /// any type with .square (CSRC), .rect (CSR tail, local columns) and .m.
     template <class R, class S, std::enable_if_t<has_square<R>::value, int> = 0>
-    ParallelSpmv(const R& r, const S& s) : n_(r.square.n) {
+    ParallelSpmv(const R& r, const S& s)
+        : n_(r.square.n), x_len_(static_cast<int64_t>(r.m)), strategy_(detail::strategy_out(s)) {
         const csrc_host_matrix m = view(r.square);
         const csrc_gpu_strategy st = Strategy(s).c();
         std::vector<int32_t> rp(r.rect.row_ptr.begin(), r.rect.row_ptr.end());
         std::vector<int32_t> ci(r.rect.col_idx.begin(), r.rect.col_idx.end());
         check(csrc_gpu_plan_create_rect(&m, &st, static_cast<int32_t>(r.m), rp.data(), ci.data(),
                                         r.rect.values.data(), &plan_));
+        default_plans(m, st);
     }
 
-    /// Explicit plan: a csrc::ColorfulPlan (has .coloring) or a
-    /// csrc::LocalBuffersPlan (has .partition), parallel.hpp:158-166.
+    /// Explicit plan: a ColorfulPlan (has .coloring) or a LocalBuffersPlan (has
+    /// .partition), parallel.hpp:158-166; with a CsrcRectMatrix, :173-181.
     template <class M, class S, class Plan>
-    ParallelSpmv(const M& a, const S& s, const Plan& plan) : n_(a.n) {
-        const csrc_host_matrix m = view(a);
+    ParallelSpmv(const M& a, const S& s, const Plan& plan) : strategy_(detail::strategy_out(s)) {
         const csrc_gpu_strategy st = Strategy(s).c();
-        if constexpr (requires_coloring<Plan>::value) {
-            std::vector<int32_t> color(plan.coloring.color.begin(), plan.coloring.color.end());
-            check(csrc_gpu_plan_create_colored(&m, &st, color.data(), plan.coloring.n_colors, &plan_));
+        std::vector<int32_t> color, starts;
+        const int32_t* cp = nullptr;
+        const int32_t* bp = nullptr;
+        int32_t nc = 0, bands = 0;
+        if constexpr (detail::has_coloring<Plan>::value) {
+            color.assign(plan.coloring.color.begin(), plan.coloring.color.end());
+            cp = color.data();
+            nc = plan.coloring.n_colors;
+            color_plan_ = detail::colorful_plan_copy(plan);
         } else {
-            const auto& bs = plan.partition.block_start;
-            std::vector<int32_t> starts(bs.begin(), bs.end());
-            check(csrc_gpu_plan_create_partitioned(&m, &st, starts.data(), plan.partition.p, &plan_));
+            starts.assign(plan.partition.block_start.begin(), plan.partition.block_start.end());
+            bp = starts.data();
+            bands = plan.partition.p;
+            buf_plan_ = detail::buffers_plan_copy(plan);
+        }
+        if constexpr (has_square<M>::value) {
+            n_ = a.square.n;
+            x_len_ = static_cast<int64_t>(a.m);
+            const csrc_host_matrix m = view(a.square);
+            std::vector<int32_t> rp(a.rect.row_ptr.begin(), a.rect.row_ptr.end());
+            std::vector<int32_t> ci(a.rect.col_idx.begin(), a.rect.col_idx.end());
+            check(csrc_gpu_plan_create_rect_plan(&m, &st, static_cast<int32_t>(a.m), rp.data(), ci.data(),
+                                                 a.rect.values.data(), cp, nc, bp, bands, &plan_));
+        } else {
+            n_ = a.n;
+            x_len_ = a.n;
+            const csrc_host_matrix m = view(a);
+            if (cp)
+                check(csrc_gpu_plan_create_colored(&m, &st, cp, nc, &plan_));
+            else
+                check(csrc_gpu_plan_create_partitioned(&m, &st, bp, bands, &plan_));
         }
     }
 
     ParallelSpmv(const ParallelSpmv&) = delete;
     ParallelSpmv& operator=(const ParallelSpmv&) = delete;
-    ParallelSpmv(ParallelSpmv&& o) noexcept : plan_(o.plan_), n_(o.n_), timings_(o.timings_) {
+    ParallelSpmv(ParallelSpmv&& o) noexcept
+        : plan_(o.plan_), n_(o.n_), x_len_(o.x_len_), timings_(o.timings_), strategy_(std::move(o.strategy_)),
+          buf_plan_(std::move(o.buf_plan_)), color_plan_(std::move(o.color_plan_)) {
         o.plan_ = nullptr;
     }
     ~ParallelSpmv() { csrc_gpu_plan_destroy(plan_); }
@@ -161,7 +359,10 @@ public:
         check(csrc_gpu_spmv(plan_, x.data(), static_cast<int64_t>(x.size()), y.data()));
         csrc_gpu_timings t;
         check(csrc_gpu_last_timings(plan_, &t));
-        timings_ = {t.init_ms / 1e3, t.compute_ms / 1e3, t.accumulate_ms / 1e3};
+        timings_ = PhaseTimings{};
+        timings_.init_max = t.init_ms / 1e3;
+        timings_.compute_max = t.compute_ms / 1e3;
+        timings_.accumulate_max = t.accumulate_ms / 1e3;
     }
 
     Vector apply_transpose(const Vector& x) {
@@ -183,6 +384,11 @@ public:
         return info.buffers_allocated;
     }
 
+    /// parallel.hpp:224-226
+    const StrategyOut& strategy() const { return strategy_; }
+    const BuffersPlanOut& buffers_plan() const { return buf_plan_; }
+    const ColorfulPlanOut& colorful_plan() const { return color_plan_; }
+
     csrc_gpu_plan_info info() const {
         csrc_gpu_plan_info i;
         check(csrc_gpu_plan_get_info(plan_, &i));
@@ -190,24 +396,35 @@ public:
     }
 
 private:
-    template <class P, class = void>
-    struct requires_coloring : std::false_type {};
-    template <class P>
-    struct requires_coloring<P, std::void_t<decltype(std::declval<P>().coloring)>> : std::true_type {};
+    // the plans the reference's build_default_plan (parallel.hpp:236-242) would
+    // hold: local buffers / colorful with p >= 2 only
+    void default_plans(const csrc_host_matrix& m, const csrc_gpu_strategy& st) {
+        if (st.p < 2) return;
+        if (st.kind == CSRC_KIND_LOCAL_BUFFERS) buf_plan_ = detail::build_buffers_plan(m, st.p);
+        if (st.kind == CSRC_KIND_COLORFUL) color_plan_ = detail::colorful_plan_of(plan_, m, st.p);
+    }
 
     csrc_gpu_plan_t plan_ = nullptr;
     int32_t n_ = 0;
-    PhaseTimings timings_;
+    int64_t x_len_ = 0;
+    PhaseTimings timings_{};
+    StrategyOut strategy_{};
+    BuffersPlanOut buf_plan_{};
+    ColorfulPlanOut color_plan_{};
 };
 
 /// spmv_csrc (kernels.hpp:25-43) on the GPU.
+/// One shot, no plan: the CSRC arrays stream to the device as stored
+/// (csrc_gpu_spmv_oneshot); repeated products should keep a ParallelSpmv.
 template <class M>
 Vector spmv_csrc(const M& a, const Vector& x) {
     if (static_cast<long long>(x.size()) != a.n)
         throw Error("spmv_csrc: x has length " + std::to_string(x.size()) + ", expected " +
                     std::to_string(a.n));
-    ParallelSpmv ex(a, Strategy());
-    return ex.apply(x);
+    const csrc_host_matrix m = view(a);
+    Vector y(static_cast<size_t>(a.n));
+    check(csrc_gpu_spmv_oneshot(&m, x.data(), static_cast<int64_t>(x.size()), y.data(), 0, 0));
+    return y;
 }
 
 /// spmv_csrc_transpose (kernels.hpp:47-65) on the GPU.
@@ -216,8 +433,10 @@ Vector spmv_csrc_transpose(const M& a, const Vector& x) {
     if (static_cast<long long>(x.size()) != a.n)
         throw Error("spmv_csrc_transpose: x has length " + std::to_string(x.size()) +
                     ", expected " + std::to_string(a.n));
-    ParallelSpmv ex(a, Strategy());
-    return ex.apply_transpose(x);
+    const csrc_host_matrix m = view(a);
+    Vector y(static_cast<size_t>(a.n));
+    check(csrc_gpu_spmv_oneshot(&m, x.data(), static_cast<int64_t>(x.size()), y.data(), 1, 0));
+    return y;
 }
 
 /// spmv_parallel (parallel.hpp:449-454).

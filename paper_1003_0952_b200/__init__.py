@@ -7,7 +7,7 @@ over the C-ABI library ``libcsrc_b200.so`` (include/csrc_gpu.h):
 reference (file:line)                  here
 =====================================  =============================================
 ``csrc::CsrcMatrix`` csrc_matrix.hpp:14  :class:`CsrcMatrix`
-``spmv_csrc`` kernels.hpp:25-43          :func:`spmv_csrc` (GPU, windowed kernel)
+``spmv_csrc`` kernels.hpp:25-43          :func:`spmv_csrc` (GPU, plan-free one-shot stream)
 ``spmv_csrc_transpose`` kernels.hpp:47   :func:`spmv_csrc_transpose`
 ``Strategy`` parallel.hpp:19-23          :class:`Strategy`
 ``ParallelSpmv`` parallel.hpp:151-446    :class:`GpuSpmv` (``ParallelSpmv`` alias)
@@ -16,12 +16,12 @@ reference (file:line)                  here
 ``partition_by_nnz`` partition.hpp:55    :func:`partition_by_nnz`
 ``effective_ranges`` partition.hpp:104   :func:`effective_ranges`
 ``build_interval_plan`` partition.hpp:113 :func:`build_interval_plan`
-``color_rows`` coloring.hpp:255          :func:`color_rows`
-``validate_coloring`` coloring.hpp:311   :func:`validate_coloring`
+``color_rows`` coloring.hpp:119-164      :func:`color_rows`
+``validate_coloring`` coloring.hpp:175   :func:`validate_coloring`
 ``ColorfulPlan`` parallel.hpp:54-94      :class:`ColorfulPlan`
 ``LocalBuffersPlan`` parallel.hpp:40-52  :class:`LocalBuffersPlan`
 ``working_set_kb`` working_set.hpp:17    :func:`working_set_kb`
-``count_ops`` cost_model.hpp:67          :func:`model_flops`
+``count_ops`` cost_model.hpp:20-42       :func:`model_flops`
 ``build_csr`` csr.hpp:55-92              :func:`build_csr` (device, construct.py)
 ``csr_to_csrc`` csrc_matrix.hpp:44-91    :func:`csr_to_csrc`, :func:`build_csrc`
 ``decompose_rect`` csrc_matrix.hpp:113   :func:`decompose_rect`
@@ -206,7 +206,7 @@ def model_bytes(a: CsrcMatrix, dtype: DType = DType.f64) -> int:
 
 
 def model_flops(a: CsrcMatrix) -> int:
-    """count_ops flops for csrc (cost_model.hpp:80-86): 2*nnz_full - n."""
+    """count_ops flops for csrc (cost_model.hpp:20-42, Format::csrc at :33): 2*nnz_full - n."""
     return int(L.model_flops(a.n, a.nnz_full()))
 
 
@@ -307,7 +307,7 @@ class ColoringValidity:
 
 def color_rows(a: CsrcMatrix, mode: ConflictMode = ConflictMode.neighborhood,
                order: ColorOrder = ColorOrder.natural) -> Coloring:
-    """color_rows(build_conflict_graph(a, mode), order) (coloring.hpp:229-300)."""
+    """color_rows(build_conflict_graph(a, mode), order) (coloring.hpp:93-164)."""
     color = np.zeros(max(a.n, 1), np.int32)
     nc = C.c_int32()
     _check(L.color_rows(C.byref(a._c()), int(mode), int(order), color.ctypes.data_as(L.P_i32),
@@ -390,7 +390,8 @@ class GpuSpmv:
             if plan is not None or band is not None:
                 raise Error("CSR plans take no explicit plan or band")
             self._a_n = int(a.n_rows)
-            self.strategy = strategy
+            self._strategy = strategy
+            self._plan_in = None
             self._h = C.c_void_p()
             rp = _as(a.row_ptr, np.int32)
             ci = _as(a.col_idx, np.int32)
@@ -405,21 +406,35 @@ class GpuSpmv:
         if rect is not None:
             a = rect.square
         self._a_n = a.n
-        self.strategy = strategy
+        self._a_ref = a  # buffers_plan / colorful_plan are built from it on request
+        self._strategy = strategy
+        self._plan_in = plan
         self._h = C.c_void_p()
         cm = a._c()
         s = strategy._c()
         if rect is not None:
-            # ParallelSpmv(const CsrcRectMatrix&, Strategy) (parallel.hpp:168-181)
-            if plan is not None or band is not None:
-                raise Error("rectangular plans take no explicit plan or band")
+            # ParallelSpmv(const CsrcRectMatrix&, Strategy[, plan]) (parallel.hpp:168-181)
+            if band is not None:
+                raise Error("rectangular plans take no band")
             trp = _as(rect.rect.row_ptr, np.int32)
             tci = _as(rect.rect.col_idx, np.int32)
             tva = _as(rect.rect.values, np.float64)
             self._keep_rect = (trp, tci, tva)
-            rc = L.plan_create_rect(C.byref(cm), C.byref(s), int(rect.m), trp.ctypes.data_as(L.P_i32),
-                                    tci.ctypes.data_as(L.P_i32) if tci.size else None,
-                                    tva.ctypes.data_as(L.P_f64) if tva.size else None, C.byref(self._h))
+            tp = (trp.ctypes.data_as(L.P_i32), tci.ctypes.data_as(L.P_i32) if tci.size else None,
+                  tva.ctypes.data_as(L.P_f64) if tva.size else None)
+            if plan is None:
+                rc = L.plan_create_rect(C.byref(cm), C.byref(s), int(rect.m), *tp, C.byref(self._h))
+            elif isinstance(plan, ColorfulPlan):
+                color = _as(plan.coloring.color, np.int32)
+                rc = L.plan_create_rect_plan(C.byref(cm), C.byref(s), int(rect.m), *tp,
+                                             color.ctypes.data_as(L.P_i32), plan.coloring.n_colors, None, 0,
+                                             C.byref(self._h))
+            elif isinstance(plan, LocalBuffersPlan):
+                bs = np.asarray(plan.partition.block_start, np.int32)
+                rc = L.plan_create_rect_plan(C.byref(cm), C.byref(s), int(rect.m), *tp, None, 0,
+                                             bs.ctypes.data_as(L.P_i32), plan.partition.p, C.byref(self._h))
+            else:
+                raise Error("plan must be a ColorfulPlan or LocalBuffersPlan")
         elif isinstance(plan, ColorfulPlan):
             color = _as(plan.coloring.color, np.int32)
             rc = L.plan_create_colored(C.byref(cm), C.byref(s), color.ctypes.data_as(L.P_i32),
@@ -461,6 +476,41 @@ class GpuSpmv:
     def buffers_allocated(self) -> int:
         """ParallelSpmv::buffers_allocated (parallel.hpp:223)."""
         return self.info().buffers_allocated
+
+    def strategy(self) -> Strategy:
+        """ParallelSpmv::strategy (parallel.hpp:224)."""
+        return self._strategy
+
+    def _active(self) -> bool:
+        s = self._strategy
+        return s.kind in (StrategyKind.local_buffers, StrategyKind.colorful) and s.p >= 2
+
+    def buffers_plan(self) -> Optional["LocalBuffersPlan"]:
+        """ParallelSpmv::buffers_plan (parallel.hpp:225): the caller's plan, or the
+        one build_default_plan (parallel.hpp:236-242) makes; None when inactive."""
+        if isinstance(self._plan_in, LocalBuffersPlan):
+            return self._plan_in
+        if self._strategy.kind != StrategyKind.local_buffers or not self._active():
+            return None
+        if not hasattr(self, "_bp"):
+            self._bp = LocalBuffersPlan.build(self._a_ref, self._strategy.p)
+        return self._bp
+
+    def colorful_plan(self) -> Optional["ColorfulPlan"]:
+        """ParallelSpmv::colorful_plan (parallel.hpp:226): the colouring the plan runs,
+        sliced for p workers (ColorfulPlan::slice, parallel.hpp:69-93)."""
+        if isinstance(self._plan_in, ColorfulPlan):
+            return self._plan_in
+        if self._strategy.kind != StrategyKind.colorful or not self._active():
+            return None
+        if not hasattr(self, "_cp"):
+            nc = C.c_int32()
+            _check(L.plan_get_coloring(self._h, None, C.byref(nc)))
+            color = np.zeros(max(self._a_n, 1), np.int32)
+            _check(L.plan_get_coloring(self._h, color.ctypes.data_as(L.P_i32), C.byref(nc)))
+            self._cp = ColorfulPlan(Coloring(color[: self._a_n], nc.value))
+            self._cp.slice(self._a_ref, self._strategy.p)
+        return self._cp
 
     def set_timing(self, on: bool = True) -> None:
         _check(L.set_timing(self._h, 1 if on else 0))
@@ -572,12 +622,23 @@ def spmv_parallel(a: CsrcMatrix, x, s: Strategy) -> Tuple[np.ndarray, PhaseTimin
         ex.close()
 
 
-def spmv_csrc(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarray:
-    """spmv_csrc (kernels.hpp:25-43) on the GPU (gather kernel, deterministic)."""
+def _oneshot(a: CsrcMatrix, xv: np.ndarray, transpose: bool, device: int) -> np.ndarray:
+    y = np.empty(a.n, np.float64)
+    _check(L.spmv_oneshot(C.byref(a._c()), xv.ctypes.data_as(L.P_f64), xv.size, y.ctypes.data_as(L.P_f64),
+                          1 if transpose else 0, device))
+    return y
+
+
+def spmv_csrc(a: CsrcMatrix, x, dtype: DType = DType.f64, device: int = 0) -> np.ndarray:
+    """spmv_csrc (kernels.hpp:25-43) on the GPU, one shot: fp64 streams the CSRC
+    arrays as stored through the plan-free path (csrc_gpu_spmv_oneshot); fp32
+    builds a plan (the one-shot path is fp64, the reference's type)."""
     xv = _as(x, np.float64)
     if xv.size != a.n:
         raise Error(f"spmv_csrc: x has length {xv.size}, expected {a.n}")
-    ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype))
+    if dtype == DType.f64:
+        return _oneshot(a, xv, False, device)
+    ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype, device=device))
     try:
         return ex.apply(xv)
     finally:
@@ -613,6 +674,8 @@ def spmv_csrc_transpose(a: CsrcMatrix, x, dtype: DType = DType.f64) -> np.ndarra
     xv = _as(x, np.float64)
     if xv.size != a.n:
         raise Error(f"spmv_csrc_transpose: x has length {xv.size}, expected {a.n}")
+    if dtype == DType.f64:
+        return _oneshot(a, xv, True, 0)
     ex = GpuSpmv(a, Strategy(StrategyKind.sequential, dtype=dtype))
     try:
         return ex.apply(xv, transpose=True)

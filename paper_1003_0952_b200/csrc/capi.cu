@@ -222,6 +222,7 @@ struct csrc_gpu_plan_s {
 
     // colorful (class-major copy)
     int n_colors = 0;
+    std::vector<int32_t> host_color;  // the colouring the plan runs (ParallelSpmv::colorful_plan)
     std::vector<count_t> class_ptr;
     DevBuf rid, cia, cja, cal, cau, cad;
     // colorful wavefront (colored.cuh): block-major / class-major renumbering, SELL-32
@@ -1901,6 +1902,7 @@ void create_typed(Plan& P, const MatView& a, const csrc_gpu_strategy& s, const C
                             std::to_string(v.row_b) + " both write y[" +
                             std::to_string(v.position) + "]");
             setup_colored<T>(P, a, color, nc);
+            P.host_color = std::move(color);
             P.launches = P.cw ? 2 : 1 + nc;  // wave: counter memset + one persistent kernel
             break;
         }
@@ -2572,6 +2574,38 @@ int csrc_gpu_plan_create_rect(const csrc_host_matrix* a, const csrc_gpu_strategy
         o.rect_val = tail_values;
         if (m_cols == 0) throw Error("ParallelSpmv: rectangular matrix needs m > n (got m=0)");
         *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_create_rect_plan(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t m_cols,
+                                   const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
+                                   const double* tail_values, const int32_t* color, int32_t n_colors,
+                                   const int32_t* block_start, int32_t bands, csrc_gpu_plan_t* out) {
+    return guarded([&] {
+        if (!out) throw Error("null output");
+        *out = nullptr;
+        if ((color != nullptr) == (block_start != nullptr))
+            throw Error("rectangular plan: pass exactly one of a colouring or a band partition");
+        CreateOpts o;
+        o.m_cols = m_cols;
+        o.rect_ptr = tail_row_ptr;
+        o.rect_col = tail_col_idx;
+        o.rect_val = tail_values;
+        o.color = color;
+        o.n_colors = n_colors;
+        o.block_start = block_start;
+        o.bands = bands;
+        if (m_cols == 0) throw Error("ParallelSpmv: rectangular matrix needs m > n (got m=0)");
+        *out = create_plan(a, s, o);
+    });
+}
+
+int csrc_gpu_plan_get_coloring(csrc_gpu_plan_t plan, int32_t* color, int32_t* n_colors) {
+    return guarded([&] {
+        Plan& P = *checked(plan);
+        if (n_colors) *n_colors = P.n_colors;
+        if (color && !P.host_color.empty())
+            std::memcpy(color, P.host_color.data(), P.host_color.size() * sizeof(int32_t));
     });
 }
 

@@ -348,7 +348,7 @@ void conflict_edge_counts(const MatView& a, int mode, count_t* n_direct, count_t
     *n_indirect = total / 2 - a.k;
 }
 
-// --- coloring.hpp:311-334 validate_coloring (same first-violation report)
+// --- coloring.hpp:175-198 validate_coloring (same first-violation report)
 Validity validate_coloring(const MatView& a, const int32_t* color, int n_colors) {
     Validity v;
     const index_t n = a.n;
@@ -516,7 +516,7 @@ int64_t csrc_model_bytes(int64_t n, int64_t nnz_stored, int32_t value_symmetric,
     return 10 * nnz_stored + 18 * n + 4;
 }
 
-// cost_model.hpp:80-86: csrc / csrc_sym flops = 2*nnz_full - n
+// cost_model.hpp:20-42 (csrc / csrc_sym at :33, :37): flops = 2*nnz_full - n
 int64_t csrc_model_flops(int64_t n, int64_t nnz_full) { return 2 * nnz_full - n; }
 
 }  // extern "C"

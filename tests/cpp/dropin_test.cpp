@@ -7,7 +7,7 @@
 #include <cstdio>
 
 #include "csrc/csrc.hpp"
-#define CSRC_GPU_ERROR_TYPE csrc::Error
+#define CSRC_GPU_REFERENCE_TYPES  // the reference's Error / PhaseTimings / Strategy / plan types
 #include "csrc_gpu.hpp"
 
 using namespace csrc;
@@ -86,6 +86,75 @@ int main() {
         CsrMatrix full = build_csr(generate_random_sym(300, 0.04, 5));
         Vector x = bench_source_vector(300);
         worst = std::max(worst, max_rel(gpu::spmv_csr(full, x), spmv_csr(full, x)));
+    }
+    // every public ParallelSpmv member (parallel.hpp:153-226) against the reference executor
+    {
+        CsrcMatrix c = csr_to_csrc(build_csr(generate_random_sym(500, 0.03, 31)));
+        Vector x = bench_source_vector(500);
+        for (AccumMethod acc : {AccumMethod::effective, AccumMethod::interval}) {
+            Strategy s{StrategyKind::local_buffers, acc, 4};
+            ParallelSpmv ref_ex(c, s);
+            gpu::ParallelSpmv ex(c, s);
+            Vector y;
+            ex.apply(x, y);  // void apply(const Vector&, Vector&) resizes y
+            worst = std::max(worst, max_rel(y, ref_ex.apply(x)));
+            csrc::PhaseTimings t = ex.last_timings();  // the reference's own type
+            if (t.compute_max <= 0.0) ++fails;
+            const Strategy& st = ex.strategy();  // the reference's own type
+            if (st.kind != s.kind || st.accum != s.accum || st.p != s.p) ++fails;
+            const LocalBuffersPlan& bp = ex.buffers_plan();
+            const LocalBuffersPlan& rbp = ref_ex.buffers_plan();
+            if (bp.partition.block_start != rbp.partition.block_start ||
+                bp.partition.block_nnz != rbp.partition.block_nnz || bp.ranges.size() != rbp.ranges.size() ||
+                bp.intervals.boundaries != rbp.intervals.boundaries ||
+                bp.intervals.intervals.size() != rbp.intervals.intervals.size())
+                ++fails;
+            for (size_t q = 0; q < bp.ranges.size() && q < rbp.ranges.size(); ++q)
+                if (bp.ranges[q].lo != rbp.ranges[q].lo || bp.ranges[q].hi != rbp.ranges[q].hi) ++fails;
+            for (size_t q = 0; q < bp.intervals.intervals.size() && q < rbp.intervals.intervals.size(); ++q)
+                if (bp.intervals.intervals[q].contributors != rbp.intervals.intervals[q].contributors) ++fails;
+            if (ex.buffers_allocated() != ref_ex.buffers_allocated()) ++fails;
+            if (!ex.colorful_plan().coloring.color.empty()) ++fails;
+        }
+        {
+            Strategy s{StrategyKind::colorful, AccumMethod::effective, 3};
+            ParallelSpmv ref_ex(c, s);
+            gpu::ParallelSpmv ex(c, s);
+            worst = std::max(worst, max_rel(ex.apply(x), ref_ex.apply(x)));
+            const ColorfulPlan& cp = ex.colorful_plan();
+            const ColorfulPlan& rcp = ref_ex.colorful_plan();
+            if (cp.coloring.color != rcp.coloring.color || cp.coloring.n_colors != rcp.coloring.n_colors ||
+                cp.coloring.classes != rcp.coloring.classes || cp.class_slices != rcp.class_slices)
+                ++fails;
+            if (!validate_coloring(c, cp.coloring).valid) ++fails;
+            if (ex.buffers_allocated() != 0 || !ex.buffers_plan().partition.block_start.empty()) ++fails;
+        }
+        {   // sequential: no plans, no buffers (parallel.hpp:197-202)
+            gpu::ParallelSpmv ex(c, Strategy{});
+            worst = std::max(worst, max_rel(ex.apply(x), spmv_csrc(c, x)));
+            if (ex.buffers_allocated() != 0 || ex.strategy().kind != StrategyKind::sequential) ++fails;
+        }
+    }
+    // rectangular + explicit plan constructors (parallel.hpp:173-181)
+    {
+        const index_t n = 150, extra = 9;
+        TripletMatrix t = generate_random_sym(n, 0.05, 77);
+        t.n_cols = n + extra;
+        for (index_t i = 0; i < n; i += 2) t.add(i, n + (i % extra), -0.5 + 0.1 * (i % 7));
+        CsrcRectMatrix r = decompose_rect(build_csr(t));
+        Vector x = bench_source_vector(n + extra);
+        Vector ref = spmv_csrc_rect(r, x);
+        Strategy sl{StrategyKind::local_buffers, AccumMethod::interval, 3};
+        gpu::ParallelSpmv e1(r, sl, LocalBuffersPlan::build(r.square, 3));
+        worst = std::max(worst, max_rel(e1.apply(x), ref));
+        if (e1.buffers_plan().partition.p != 3) ++fails;
+        Strategy sc{StrategyKind::colorful, AccumMethod::effective, 2};
+        ColorfulPlan cp = ColorfulPlan::build(r.square, 2);
+        gpu::ParallelSpmv e2(r, sc, cp);
+        worst = std::max(worst, max_rel(e2.apply(x), ref));
+        if (e2.colorful_plan().coloring.color != cp.coloring.color) ++fails;
+        ParallelSpmv ref_e2(r, sc, cp);
+        worst = std::max(worst, max_rel(e2.apply(x), ref_e2.apply(x)));
     }
     // error behaviour: the reference's csrc::Error with its wording
     try {
