@@ -277,184 +277,147 @@ def workload_config(args, a, world):
     return workload_config_plain(args, a, P.model_bytes(a), world)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
-    ap.add_argument("--kind", default="gather", choices=["gather", "windowed", "atomic", "colorful", "local_buffers"])
-    ap.add_argument("--compare", default="gather_explicit,windowed,atomic",
-                    help="other kernels timed on the same workload (reported under 'kernels'); '' = none")
-    ap.add_argument("--flush-mb", type=int, default=256)
-    ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample budget")
-    args = ap.parse_args()
-    world, rank, local = dist_env()
-    if args.impl == "reference":
-        return run_reference_arm(args, world, rank)
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
 
-    import torch
-    import paper_1003_0952_b200 as P
 
-    # CSRC_BENCH_SHARE_GPU=1 (functional check of the N>1 code path on a one-GPU box, gather bands only:
-    # their kernels never wait on each other): ranks share the visible GPUs and the timing collectives
-    # run over gloo. Its numbers are not measurements.
-    share = os.environ.get("CSRC_BENCH_SHARE_GPU") == "1"
-    if share:
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dist = None
-    coll_dev = "cpu" if share else "cuda"
-    if world > 1:
-        import torch.distributed as dist
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+KERNEL_NAMES = {1: "k_gather_rows", 2: "k_gather_staged", 3: "k_gather_sell"}
+
+
+def kernel_name(info, kind):
+    if kind == "gather":
+        return KERNEL_NAMES.get(int(info.gather_form), "k_gather")
+    return {"windowed": "k_windowed", "atomic": "k_atomic", "colorful": "k_colored_wave",
+            "local_buffers": "k_windowed (+ spill init / accumulate)"}[kind]
+
+
+def time_plan(P, a, strat, xd, yd, steps, flush, warm=3, env=None):
+    """Device-resident products of one plan: mean step / kernel ms (CUDA events on
+    the plan's stream), the plan info."""
+    old = {}
+    for k, v in (env or {}).items():
+        old[k] = os.environ.get(k)
+        os.environ[k] = v
+    try:
+        ex = P.GpuSpmv(a, strat)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    for _ in range(warm):
+        ex.apply_device(xd, yd)
+    tot, ker = ex.time_products(xd, yd, steps, flush)
+    info = ex.info()
+    ex.close()
+    return float(np.mean(tot)), float(np.mean(ker)), info
+
+
+def run_single(args, P, torch, local):
     dtype = P.DType.f32 if args.dtype == "f32" else P.DType.f64
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     a, x, _ = P.config_matrix(args.config)
     mb = P.model_bytes(a, dtype)
     flops = 2 * a.nnz_full()
-    kind = P.StrategyKind[args.kind]
-    strat = P.Strategy(kind, P.AccumMethod.interval, p=8, dtype=dtype, device=local)
+    strat = P.Strategy(P.StrategyKind[args.kind], P.AccumMethod.interval, p=8, dtype=dtype, device=local)
     flush = 0 if mb > 400e6 else args.flush_mb << 20
-
-    if world == 1:
-        ex = P.GpuSpmv(a, strat)
-        xd = torch.from_numpy(x).to(device="cuda", dtype=tdt)
-        yd = torch.zeros_like(xd)
-        for _ in range(args.warmup):
-            ex.apply_device(xd, yd)
-        torch.cuda.synchronize()
-        with ClockSampler(local) as cs:
-            tot, ker = ex.time_products(xd, yd, args.steps, flush)
-            torch.cuda.synchronize()
-        clocks = cs.summary()
-        ms = float(np.mean(tot))
-        kms = float(np.mean(ker))
-        info = ex.info()
-        layout_bytes, row_patterns = int(info.stream_bytes), int(info.row_patterns)
-        kernel_name = {1: "k_gather_rows", 2: "k_gather_staged", 3: "k_gather_sell"}.get(
-            int(info.gather_form), {"windowed": "k_windowed", "atomic": "k_atomic"}.get(args.kind, args.kind))
-        # our kernels per product (the y memset of windowed/atomic is a driver memset, not counted)
-        launches_per_step = 1 if args.kind in ("gather", "windowed", "atomic") else info.launches_per_apply
-        others = {}
-        for name in [k for k in args.compare.split(",") if k and k != args.kind]:
-            # gather_explicit: the gather kernel with explicit column indices (row-pattern form off)
-            env_off = name == "gather_explicit"
-            if env_off:
-                os.environ["CSRC_GPU_GPATTERN"] = "0"
-            ox = P.GpuSpmv(a, P.Strategy(P.StrategyKind["gather" if env_off else name], P.AccumMethod.interval,
-                                          p=8, dtype=dtype, device=local))
-            if env_off:
-                del os.environ["CSRC_GPU_GPATTERN"]
-            for _ in range(3):
-                ox.apply_device(xd, yd)
-            otot, oker = ox.time_products(xd, yd, min(args.steps, 50), flush)
-            ox.close()
-            oms = float(np.mean(otot))
-            okms = float(np.mean(oker))
-            peak_o, _ = load_peaks()
-            others[name] = dict(ms_per_step=oms, gflops=flops / (oms / 1e3) / 1e9,
-                                effective_gbs=mb / (oms / 1e3) / 1e9, kernel_ms=okms,
-                                roofline_achieved_gbs=mb / (okms / 1e3) / 1e9,
-                                roofline_frac=mb / (okms / 1e3) / 1e9 / peak_o,
-                                reads_csrc_as_stored=name in ("windowed", "atomic"))
-        # end to end through the public host API: pinned x -> device, product, y -> pinned host
-        xh = torch.from_numpy(x).pin_memory()
-        yh = torch.empty_like(xh).pin_memory()
-        ex.apply(xh.numpy(), yh.numpy())
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            ex.apply(xh.numpy(), yh.numpy())
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        ex.close()
-        ms_max = ms
-    else:
-        others = {}
-        layout_bytes, row_patterns = None, 0
-        kernel_name = "k_gather_staged" if args.kind == "gather" else "k_" + args.kind
-        from paper_1003_0952_b200.dist import DistSpmv
-        ds = DistSpmv(a, strat)
-        p = ds.plan
-        xd = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).to(device="cuda", dtype=tdt)
-        yd = torch.zeros(p.row_end - p.y_lo, device="cuda", dtype=tdt)
-        dist.barrier()
-        for _ in range(args.warmup):
-            ds.apply_device(xd, yd)
-        torch.cuda.synchronize()
-        dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(local) as cs:
-            e0.record()
-            for _ in range(args.steps):
-                ds.apply_device(xd, yd)
-            e1.record()
-            torch.cuda.synchronize()
-        dist.barrier()
-        clocks = cs.summary()
-        ms = e0.elapsed_time(e1) / args.steps
-        t = torch.tensor([ms], device=coll_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
-        kms = ms
-        launches_per_step = 1 if p.mode == "gather" else 3 + len(p.recvs)
-        # e2e: host slice in, owned rows out
-        xh = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).pin_memory()
-        yh = torch.empty(p.row_end - p.row_begin, dtype=torch.float64).pin_memory()
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            xd.copy_(xh.to(tdt), non_blocking=True)
-            ds.apply_device(xd, yd)
-            yh.copy_(yd[p.row_begin - p.y_lo:].to(torch.float64), non_blocking=True)
-            torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        te = torch.tensor([e2e_s], device=coll_dev)
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_s = float(te.item())
-        ds.close()
-
-    if rank != 0:
-        if dist is not None:
-            dist.destroy_process_group()
-        return 0
     peak, peak_src = load_peaks()
-    gbs = mb / (ms_max / 1e3) / 1e9
-    achieved = mb / (kms / 1e3) / 1e9
-    elem = 4 if args.dtype == "f32" else 8
-    wl = f"{args.config}-{args.dtype}-{args.kind}"
+
+    ex = P.GpuSpmv(a, strat)
+    xd = torch.from_numpy(x).to(device="cuda", dtype=tdt)
+    yd = torch.zeros_like(xd)
+    for _ in range(args.warmup):
+        ex.apply_device(xd, yd)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as cs:
+        tot, ker = ex.time_products(xd, yd, args.steps, flush)
+        torch.cuda.synchronize()
+    clocks = cs.summary()
+    ms, kms = float(np.mean(tot)), float(np.mean(ker))
+    info = ex.info()
+    layout_bytes, row_patterns = int(info.stream_bytes), int(info.row_patterns)
+    kname = kernel_name(info, args.kind)
+    # our kernels per product (driver memsets not counted)
+    launches_per_step = {"gather": 1, "windowed": 1, "atomic": 1, "colorful": 1}.get(args.kind, 3)
+
+    # end to end through the public host API (GpuSpmv.apply -> csrc_gpu_spmv): x in, y out every step
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    ex.apply(xh.numpy(), yh.numpy())
+    e2e_steps = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ex.apply(xh.numpy(), yh.numpy())
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    # the reference API's own call shape: pageable std::vector-like numpy x and y (y reused, as
+    # run_benchmark's apply(x, y) loop does, bench.hpp:225-255)
+    xp = np.array(x)
+    yp = np.empty_like(xp)
+    ex.apply(xp, yp)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        ex.apply(xp, yp)
+    e2e_pageable_s = (time.perf_counter() - t0) / e2e_steps
+    ex.close()
+
+    # the other kernels on the same workload
+    others = {}
+    specs = {
+        "gather_explicit": (P.Strategy(P.StrategyKind.gather, dtype=dtype, device=local), {"CSRC_GPU_GPATTERN": "0"}),
+        "windowed": (P.Strategy(P.StrategyKind.windowed, dtype=dtype, device=local), None),
+        "atomic": (P.Strategy(P.StrategyKind.atomic, dtype=dtype, device=local), None),
+        "colorful": (P.Strategy(P.StrategyKind.colorful, p=8, dtype=dtype, device=local), None),
+        "local_buffers": (P.Strategy(P.StrategyKind.local_buffers, P.AccumMethod.interval, p=8, dtype=dtype,
+                                     device=local), None),
+    }
+    for name in [k for k in args.compare.split(",") if k and k != args.kind]:
+        st, env = specs[name]
+        oms, okms, oinf = time_plan(P, a, st, xd, yd, min(args.steps, 50), flush, env=env)
+        others[name] = dict(ms_per_step=oms, gflops=flops / (oms / 1e3) / 1e9, kernel_ms=okms,
+                            effective_gbs=mb / (okms / 1e3) / 1e9, frac_of_model_roofline=mb / (okms / 1e3) / 1e9 / peak,
+                            stream_bytes=int(oinf.stream_bytes),
+                            reads_csrc_as_stored=name in ("windowed", "atomic", "local_buffers"),
+                            layout=("CSRC arrays as stored" if name in ("windowed", "atomic", "local_buffers") else
+                                    "CSRC pairs class-major (colour classes), renumbered" if name == "colorful" else
+                                    "per-row entry streams (CSR re-layout at plan time)"))
+    wall = others.get("windowed")
+    achieved = layout_bytes / (kms / 1e3) / 1e9
+    roofline = dict(
+        bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
+        traffic=load_traffic(f"{args.config}-{args.dtype}-{args.kind}"), peak_source=peak_src, kernel=kname,
+        kernel_ms=kms, algorithmic_bytes_per_launch=layout_bytes,
+        bytes_basis=("the bytes this plan's kernel streams per product (info.stream_bytes): "
+                     + ("the CSRC pairs re-laid out at plan time as per-row entry streams with "
+                        f"{'27 row patterns instead of column indices' if row_patterns else 'explicit columns'}"
+                        if args.kind == "gather" else "the CSRC working-set model (working_set.hpp:11-23)")),
+        csrc_model=dict(bytes=mb, effective_gbs=mb / (kms / 1e3) / 1e9,
+                        note="reference working-set bytes (10 nnz + 18 n + 4) / kernel time; an effective "
+                             "bandwidth, above the peak when the layout moves fewer bytes than the model"),
+        row_patterns=row_patterns)
+    if wall:
+        roofline["csrc_as_stored"] = dict(
+            kernel="k_windowed", kernel_ms=wall["kernel_ms"], bytes=mb,
+            achieved=mb / (wall["kernel_ms"] / 1e3) / 1e9, frac=mb / (wall["kernel_ms"] / 1e3) / 1e9 / peak,
+            note="the CSRC roofline: the kernel that streams ja/al/au/ad/ia as stored (TMA tiles, red.global "
+                 "scatter), model bytes / its kernel time")
     line = dict(
-        metric=METRIC, value=flops / (ms_max / 1e3) / 1e9, unit="GFLOP/s", n_gpus=world, steps=args.steps,
-        warmup=args.warmup, ms_per_step=ms_max, higher_is_better=True,
-        scaling="strong", vs_baseline=None, dtype=args.dtype,
-        data="synthetic (BASELINE config, seeded fixture, DESIGN.md Fixtures)",
-        config=workload_config(args, a, world),
-        effective_gbs=gbs, roofline_frac_of_measured_hbm=gbs / peak,
-        gflops_true=(flops - a.n) / (ms_max / 1e3) / 1e9,
-        roofline=dict(bound="hbm", achieved=achieved, peak=peak, unit="GB/s", frac=achieved / peak,
-                      traffic=load_traffic(wl) if world == 1 else None, peak_source=peak_src,
-                      kernel=kernel_name,
-                      algorithmic_bytes_per_launch=mb, kernel_ms=kms,
-                      layout_bytes_per_launch=layout_bytes,
-                      layout_frac=(layout_bytes / (kms / 1e3) / 1e9) / peak if layout_bytes else None,
-                      row_patterns=row_patterns),
-        e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8 if world == 1
-                 else (p.x_hi - p.x_lo) * 8, d2h_bytes_per_step=a.n * 8 if world == 1
-                 else (p.row_end - p.row_begin) * 8, wall_ms_per_step=e2e_s * 1e3),
-        gpu_launches=launches_per_step * args.steps,
-        clocks=clocks,
-    )
+        metric=METRIC, value=flops / (ms / 1e3) / 1e9, unit="GFLOP/s", n_gpus=1, steps=args.steps,
+        warmup=args.warmup, ms_per_step=ms, higher_is_better=True, scaling=bench_scaling(args),
+        vs_baseline=None, dtype=args.dtype, data="synthetic (BASELINE config, seeded fixture, DESIGN.md Fixtures)",
+        config=workload_config(args, a, 1), effective_gbs=mb / (ms / 1e3) / 1e9,
+        gflops_true=(flops - a.n) / (ms / 1e3) / 1e9, roofline=roofline,
+        e2e=dict(value=flops / e2e_s / 1e9, unit="GFLOP/s", h2d_bytes_per_step=a.n * 8, d2h_bytes_per_step=a.n * 8,
+                 wall_ms_per_step=e2e_s * 1e3, api="GpuSpmv.apply (csrc_gpu_spmv), pinned host x / y",
+                 pageable=dict(value=flops / e2e_pageable_s / 1e9, wall_ms_per_step=e2e_pageable_s * 1e3,
+                               api="GpuSpmv.apply with pageable numpy x / y (std::vector shape), y reused")),
+        gpu_launches=launches_per_step * args.steps, clocks=clocks)
     if others:
         line["kernels"] = others
-    if world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         a_c, x_c, _ = oracle_side_fixture(args)
         res = cpu_reference_suite(a_c, x_c, args.cpu_seconds)
         del a_c, x_c
@@ -465,9 +428,147 @@ def main():
                     f"p = {res['cores']} of {res['host']['physical']} physical cores / "
                     f"{res['host']['logical']} logical CPUs); {res['lib']}"),
             methods=res["methods"], sequential_gflops=res["seq_gflops"], host=res["host"])
-    print(json.dumps(line), flush=True)
-    if dist is not None:
+    return line
+
+
+def run_multi(args, P, torch, world, rank, local, share):
+    """N > 1: the matrix in N partition_by_nnz row bands, one per rank; every timed
+    step includes the exchange of the band form:
+      gather   -- x-halo refresh (grouped NCCL send/recv of the rows other bands read,
+                  overlapped with the interior rows), then the boundary rows;
+      windowed -- boundary rows, y-halo partials shipped to their owners with grouped
+                  NCCL send/recv while the interior rows run, then the halo reduce.
+    The primary form is --kind (gather or windowed); the other is timed too ("forms")."""
+    import torch.distributed as dist
+    from paper_1003_0952_b200.dist import DistSpmv
+    dtype = P.DType.f32 if args.dtype == "f32" else P.DType.f64
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    a, x, _ = P.config_matrix(args.config)
+    mb = P.model_bytes(a, dtype)
+    flops = 2 * a.nnz_full()
+    coll_dev = "cpu" if share else "cuda"
+    primary = "windowed" if args.kind == "windowed" else "gather"
+    forms = {}
+    clocks = None
+    for form in [primary] + [f for f in ("gather", "windowed") if f != primary]:
+        ds = DistSpmv(a, P.Strategy(P.StrategyKind[form], dtype=dtype, device=local))
+        p = ds.plan
+        xd = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).to(device="cuda", dtype=tdt)
+        yd = torch.zeros(p.row_end - p.y_lo, device="cuda", dtype=tdt)
+        refresh = form == "gather"
+        dist.barrier()
+        for _ in range(args.warmup):
+            ds.apply_device(xd, yd, refresh_x=refresh)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as cs:
+            e0.record()
+            for _ in range(args.steps):
+                ds.apply_device(xd, yd, refresh_x=refresh)
+            e1.record()
+            torch.cuda.synchronize()
+        dist.barrier()
+        if clocks is None:
+            clocks = cs.summary()
+        t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        # e2e: this rank's x slice in (pinned), its owned y rows out, every step
+        xh = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).pin_memory()
+        yh = torch.empty(p.row_end - p.row_begin, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e2e_steps = max(3, min(args.steps, 50))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            xd.copy_(xh.to(tdt), non_blocking=True)
+            ds.apply_device(xd, yd, refresh_x=refresh)
+            yh.copy_(yd[p.row_begin - p.y_lo:].to(torch.float64), non_blocking=True)
+            torch.cuda.synchronize()
+        te = torch.tensor([(time.perf_counter() - t0) / e2e_steps], device=coll_dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        hb = torch.tensor([(p.x_hi - p.x_lo) * 8, (p.row_end - p.row_begin) * 8], device=coll_dev, dtype=torch.float64)
+        dist.all_reduce(hb)
+        halo = (sum(q1 - q0 for _, q0, q1 in p.x_sends) + sum(q1 - q0 for _, q0, q1 in p.x_recvs) if refresh else
+                sum(q1 - q0 for _, q0, q1 in p.sends) + sum(q1 - q0 for _, q0, q1 in p.recvs))
+        forms[form] = dict(ms_per_step=ms, gflops=flops / (ms / 1e3) / 1e9, effective_gbs=mb / (ms / 1e3) / 1e9,
+                           e2e_ms=float(te.item()) * 1e3, e2e_gflops=flops / float(te.item()) / 1e9,
+                           h2d_bytes_per_step=int(hb[0].item()), d2h_bytes_per_step=int(hb[1].item()),
+                           exchange=("x halo (grouped NCCL send/recv), interior rows overlapped" if refresh else
+                                     "y halo partials to their owners (grouped NCCL send/recv), interior "
+                                     "rows overlapped, then the red.global halo reduce"),
+                           rank0_halo_elems=int(halo))
+        ds.close()
+        del xd, yd
+    f0 = forms[primary]
+    peak, peak_src = load_peaks()
+    return dict(
+        metric=METRIC, value=f0["gflops"], unit="GFLOP/s", n_gpus=world, steps=args.steps, warmup=args.warmup,
+        ms_per_step=f0["ms_per_step"], higher_is_better=True, scaling=bench_scaling(args), vs_baseline=None,
+        dtype=args.dtype, data="synthetic (BASELINE config, seeded fixture, DESIGN.md Fixtures)",
+        config=workload_config(args, a, world), effective_gbs=f0["effective_gbs"],
+        roofline=dict(bound="hbm", achieved=f0["effective_gbs"] / world, peak=peak, unit="GB/s",
+                      frac=f0["effective_gbs"] / world / peak, traffic=None, peak_source=peak_src,
+                      kernel="k_gather_staged" if primary == "gather" else "k_windowed",
+                      note="per-GPU share of the CSRC model bytes / the max-over-ranks step (exchange included)"),
+        e2e=dict(value=f0["e2e_gflops"], unit="GFLOP/s", h2d_bytes_per_step=f0["h2d_bytes_per_step"],
+                 d2h_bytes_per_step=f0["d2h_bytes_per_step"], wall_ms_per_step=f0["e2e_ms"]),
+        gpu_launches=(4 if primary == "gather" else 4) * args.steps, forms=forms, clocks=clocks,
+        shared_gpu=share or None)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--kind", default="gather", choices=["gather", "windowed", "atomic", "colorful", "local_buffers"])
+    ap.add_argument("--compare", default="gather_explicit,windowed,atomic,colorful,local_buffers",
+                    help="other kernels timed on the same workload (reported under 'kernels'); '' = none")
+    ap.add_argument("--flush-mb", type=int, default=256)
+    ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample budget")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # --gpus N launches its own N ranks (torchrun on 127.0.0.1), one per GPU
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    if world != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N ranks "
+                                                     f"for --gpus N (or omit WORLD_SIZE to self-launch)"}), flush=True)
+        return 2
+    if args.impl == "reference":
+        return run_reference_arm(args, world, rank)
+
+    import torch
+    import paper_1003_0952_b200 as P
+
+    # CSRC_BENCH_SHARE_GPU=1: a functional check of the N > 1 path on a box with fewer GPUs than ranks
+    # (ranks share the visible GPUs; collectives over gloo). Its numbers are not measurements.
+    share = os.environ.get("CSRC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local %= torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    if world == 1:
+        line = run_single(args, P, torch, local)
+    else:
+        import torch.distributed as dist
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        line = run_multi(args, P, torch, world, rank, local, share)
         dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 

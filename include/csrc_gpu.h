@@ -302,6 +302,11 @@ int csrc_partition_by_nnz(const csrc_host_matrix* a, int32_t p, int32_t* block_s
 int csrc_effective_ranges(const csrc_host_matrix* a, int32_t p, const int32_t* block_start,
                           int32_t* lo, int32_t* hi);
 
+/* Multi-GPU gather bands: x_hi[b] = one past the last row that reads x in band b
+ * (rows naming one of band b's rows as a lower column), at least block_start[b+1];
+ * band b reads x on [effective_range lo, x_hi[b]) (paper_1003_0952_b200.dist). */
+int csrc_bands_x_hi(const csrc_host_matrix* a, int32_t p, const int32_t* block_start, int32_t* x_hi);
+
 /* build_interval_plan (partition.hpp:113-134). Two-call protocol: pass NULL
  * outputs to get the sizes, then buffers of those sizes.
  * iv_begin/iv_end[n_intervals], contrib_ptr[n_intervals+1], contrib[n_contrib],

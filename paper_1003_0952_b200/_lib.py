@@ -126,6 +126,7 @@ plan_create_rect = _sig("csrc_gpu_plan_create_rect", C.c_int, PM, PS, i32, P_i32
                         C.POINTER(vp))
 plan_create_rect_plan = _sig("csrc_gpu_plan_create_rect_plan", C.c_int, PM, PS, i32, P_i32, P_i32, P_f64,
                              P_i32, i32, P_i32, i32, C.POINTER(vp))
+bands_x_hi = _sig("csrc_bands_x_hi", C.c_int, PM, i32, P_i32, P_i32)
 plan_get_coloring = _sig("csrc_gpu_plan_get_coloring", C.c_int, vp, P_i32, P_i32)
 spmv_oneshot = _sig("csrc_gpu_spmv_oneshot", C.c_int, PM, P_f64, i64, P_f64, i32, i32)
 plan_destroy = _sig("csrc_gpu_plan_destroy", None, vp)
@@ -183,7 +184,7 @@ EXPORTED = [
     "csrc_gpu_last_error", "csrc_gpu_abi_version", "csrc_gpu_device_count",
     "csrc_gpu_plan_create", "csrc_gpu_plan_create_colored", "csrc_gpu_plan_create_partitioned",
     "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_create_csr", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
-    "csrc_gpu_plan_create_rect_plan", "csrc_gpu_plan_get_coloring", "csrc_gpu_spmv_oneshot",
+    "csrc_gpu_plan_create_rect_plan", "csrc_gpu_plan_get_coloring", "csrc_gpu_spmv_oneshot", "csrc_bands_x_hi",
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
     "csrc_gpu_gather_interior", "csrc_gpu_spmv_device_rows",

@@ -422,6 +422,45 @@ int csrc_effective_ranges(const csrc_host_matrix* m, int32_t p, const int32_t* b
     });
 }
 
+int csrc_bands_x_hi(const csrc_host_matrix* m, int32_t p, const int32_t* block_start, int32_t* x_hi) {
+    return guarded([&] {
+        MatView a = view_of(m, false);
+        if (p < 1) throw Error("bands_x_hi: p must be >= 1");
+        // x_hi[b] = max(row_end_b, 1 + the last row whose lower columns fall in band b);
+        // rows scanned over threads, each keeping its own per-band maximum
+        const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+        const int T = static_cast<int>(std::max<count_t>(1, std::min<count_t>(std::min(hw, 32), a.n / 65536)));
+        std::vector<std::vector<index_t>> part(T, std::vector<index_t>(p, -1));
+        auto band_of = [&](index_t q) {
+            return static_cast<int>(std::upper_bound(block_start, block_start + p + 1, q) - block_start) - 1;
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < T; ++t)
+            pool.emplace_back([&, t] {
+                const index_t r0 = static_cast<index_t>(static_cast<count_t>(a.n) * t / T);
+                const index_t r1 = static_cast<index_t>(static_cast<count_t>(a.n) * (t + 1) / T);
+                std::vector<index_t>& mx = part[t];
+                for (index_t r = r0; r < r1; ++r)
+                    for (index_t q = a.ia[r]; q < a.ia[r + 1]; ++q) {
+                        const int b = band_of(a.ja[q]);
+                        if (b >= 0 && b < p && r > mx[b]) mx[b] = r;
+                        // columns ascend within a row: skip to the next band
+                        if (b >= 0 && b + 1 <= p) {
+                            const index_t next = block_start[b + 1];
+                            while (q + 1 < a.ia[r + 1] && a.ja[q + 1] < next) ++q;
+                        }
+                    }
+            });
+        for (auto& th : pool) th.join();
+        for (int b = 0; b < p; ++b) {
+            index_t best = block_start[b + 1];
+            for (int t = 0; t < T; ++t)
+                if (part[t][b] >= 0) best = std::max<index_t>(best, part[t][b] + 1);
+            x_hi[b] = best;
+        }
+    });
+}
+
 int csrc_interval_plan(int32_t p, const int32_t* lo, const int32_t* hi, int32_t* n_intervals,
                        int32_t* n_contrib, int32_t* n_boundaries, int32_t* iv_begin,
                        int32_t* iv_end, int32_t* contrib_ptr, int32_t* contrib,

@@ -100,14 +100,16 @@ def band_x_hi(a: CsrcMatrix, r0: int, r1: int) -> int:
 
 
 def bands_x_hi(a: CsrcMatrix, block_start: List[int]) -> List[int]:
-    """band_x_hi for every band of a partition (one pass over the pairs)."""
-    rows = np.repeat(np.arange(a.n, dtype=np.int64), np.diff(a.ia))
-    out = []
-    for b in range(len(block_start) - 1):
-        r0, r1 = block_start[b], block_start[b + 1]
-        m = (a.ja >= r0) & (a.ja < r1)
-        out.append(int(max(r1, rows[m].max() + 1)) if m.any() else int(r1))
-    return out
+    """band_x_hi for every band of a partition (csrc_bands_x_hi: one threaded
+    pass over the rows in the product library)."""
+    import ctypes as C
+    from . import _check
+    from . import _lib as L
+    p = len(block_start) - 1
+    bs = np.asarray(block_start, np.int32)
+    out = np.zeros(max(p, 1), np.int32)
+    _check(L.bands_x_hi(C.byref(a._c()), p, bs.ctypes.data_as(L.P_i32), out.ctypes.data_as(L.P_i32)))
+    return [int(v) for v in out[:p]]
 
 
 def gather_plan(a: CsrcMatrix, world: int, rank: int, x_hi: Optional[int] = None,
@@ -202,17 +204,42 @@ class DistSpmv:
             self.ex = None
 
     # -------------------------------------------------------------- exchange
+    def _staged(self) -> bool:
+        """gloo moves CPU tensors only: device slices are staged through host
+        copies (the one-GPU functional check of the N > 1 path; NCCL moves the
+        device slices directly)."""
+        if not hasattr(self, "_gloo"):
+            self._gloo = self.dist.get_backend(self.group) == "gloo"
+        return self._gloo
+
+    def _batch(self, sends, recvs):
+        """Grouped P2P: sends / recvs are (peer, tensor) lists. Returns works whose
+        wait() also lands staged receives in their device slices."""
+        dist = self.dist
+        if not self._staged() or not any(t.is_cuda for _, t in sends + recvs):
+            ops = [dist.P2POp(dist.isend, t, peer, self.group) for peer, t in sends]
+            ops += [dist.P2POp(dist.irecv, t, peer, self.group) for peer, t in recvs]
+            return dist.batch_isend_irecv(ops) if ops else []
+        hs = [(peer, t.cpu()) for peer, t in sends]
+        hr = [(peer, t, t.new_empty(t.shape, device="cpu")) for peer, t in recvs]
+        ops = [dist.P2POp(dist.isend, h, peer, self.group) for peer, h in hs]
+        ops += [dist.P2POp(dist.irecv, h, peer, self.group) for peer, _, h in hr]
+        works = dist.batch_isend_irecv(ops) if ops else []
+
+        class Landed:
+            def wait(_self):
+                for w in works:
+                    w.wait()
+                for _, dev_t, h in hr:
+                    dev_t.copy_(h)
+        return [Landed()]
+
     def _post_x(self, x_local):
         """Grouped P2P of the x halo (gather form): my rows to the peers whose
         x range covers them, the peers' rows into my halo slices."""
-        dist = self.dist
         p = self.plan
-        ops = []
-        for peer, q0, q1 in p.x_sends:
-            ops.append(dist.P2POp(dist.isend, x_local[q0 - p.x_lo:q1 - p.x_lo], peer, self.group))
-        for peer, q0, q1 in p.x_recvs:
-            ops.append(dist.P2POp(dist.irecv, x_local[q0 - p.x_lo:q1 - p.x_lo], peer, self.group))
-        return dist.batch_isend_irecv(ops) if ops else []
+        return self._batch([(peer, x_local[q0 - p.x_lo:q1 - p.x_lo]) for peer, q0, q1 in p.x_sends],
+                           [(peer, x_local[q0 - p.x_lo:q1 - p.x_lo]) for peer, q0, q1 in p.x_recvs])
 
     def exchange_x(self, x_local):
         """Blocking x-halo refresh: afterwards x_local holds current x on
@@ -222,14 +249,9 @@ class DistSpmv:
         return x_local
 
     def _post(self, y_local, recv_bufs):
-        dist = self.dist
         p = self.plan
-        ops = []
-        for peer, q0, q1 in p.sends:
-            ops.append(dist.P2POp(dist.isend, y_local[q0 - p.lo:q1 - p.lo], peer, self.group))
-        for (peer, q0, q1), buf in zip(p.recvs, recv_bufs):
-            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
-        return dist.batch_isend_irecv(ops) if ops else []
+        return self._batch([(peer, y_local[q0 - p.lo:q1 - p.lo]) for peer, q0, q1 in p.sends],
+                           [(peer, buf) for (peer, q0, q1), buf in zip(p.recvs, recv_bufs)])
 
     def apply_host(self, x_local, y_local, refresh_x: bool = False):
         """Host mode (gloo): band product via the injected callable."""

@@ -154,3 +154,13 @@ def test_gather_x_halo_lists_are_consistent():
                 covered[q0:q1] += 1
             assert np.all(covered[p.x_lo:p.x_hi] == 1)
             assert covered[:p.x_lo].sum() == 0 and covered[p.x_hi:].sum() == 0
+
+
+def test_bands_x_hi_matches_the_numpy_definition():
+    """csrc_bands_x_hi (threaded C++) equals the per-band numpy definition."""
+    from paper_1003_0952_b200.dist import band_x_hi, bands_x_hi
+    for cfg in ("c1", "c2"):
+        a, _, _ = P.config_matrix(cfg)
+        for p in (1, 2, 3, 8, 16):
+            bs = P.partition_by_nnz(a, p).block_start
+            assert bands_x_hi(a, bs) == [band_x_hi(a, bs[b], bs[b + 1]) for b in range(p)]
