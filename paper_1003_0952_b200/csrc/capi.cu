@@ -569,10 +569,11 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
     P.win_lanes = env_int("CSRC_GPU_LANES", pick_win_lanes(P.k, P.nrows, P.win_ring));
     if (P.win_lanes != 1 && P.win_lanes != 2 && P.win_lanes != 4)
         throw Error("windowed lanes per row must be 1, 2 or 4");
-    {   // ~1.7K pairs (~35 KB of fp64 matrix data) per tile: big TMA copies
+    {   // ~1.7K pairs (~35 KB of fp64 matrix data) per tile: big TMA copies, but
+        // long rows halve the tile so 2+ CTAs fit an SM (C4, 40 pairs per row: 64-row
+        // tiles 0.561 vs 0.644 ms sustained; C2/C3/C5 keep 128: profiles/r02_windowed_tiles.txt)
         const double avg = P.nrows ? static_cast<double>(P.k) / P.nrows : 0.0;
-        (void)avg;  // profiles/r01_sweep13-14: 128-row tiles win on every config
-        P.tile_rows = env_int("CSRC_GPU_TILE", 128);
+        P.tile_rows = env_int("CSRC_GPU_TILE", avg > 20.0 ? 64 : 128);
     }
     if (P.tile_rows != 32 && P.tile_rows != 64 && P.tile_rows != 128)
         throw Error("windowed tile rows must be 32, 64 or 128");
@@ -589,7 +590,9 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
     // deepest pipeline that still keeps `min_ctas` CTAs per SM
     int per_sm = 0;
     const int max_st = std::min(env_int("CSRC_GPU_STAGES", 4), dev::kMaxStages);
-    const int min_ctas = env_int("CSRC_GPU_MINCTAS", 2);
+    // 3 CTAs per SM (2 stages at C5) over 2 (3 stages): C5 sustained 0.896 vs 0.965 ms kernel
+    // (100 products; the burst sweep of round 1 had preferred 2)
+    const int min_ctas = env_int("CSRC_GPU_MINCTAS", 3);
     for (int st = max_st; st >= 2; --st) {
         P.stages = st;
         size_rings(P, st);
@@ -603,7 +606,8 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
                     " pairs exceeds the shared-memory tile budget");
     const int resident = num_sms(P.device) * per_sm;
     // run length >= stages: alternating ring banks per run (windowed.cuh)
-    const int run_len = std::max(P.stages, env_int("CSRC_GPU_RUN_LEN", 4));
+    // short runs keep all CTAs on one narrow wavefront (C5: 0.868 ms at 2 vs 0.881 at 4)
+    const int run_len = std::max(P.stages, env_int("CSRC_GPU_RUN_LEN", 2));
     std::vector<int32_t> band_first;
     std::vector<index_t> bs;
     if (banded) {
@@ -675,6 +679,7 @@ dev::WinArgs<T> win_args(const Plan& P, const void* x, void* out, bool transpose
     A.ring_near = P.ring_near;
     A.ring_far = P.ring_far;
     A.rotate = env_int("CSRC_GPU_WIN_ROTATE", 0);  // diagnostics (see windowed.cuh)
+    A.combine = env_int("CSRC_GPU_WIN_COMBINE", 0);
     A.max_tile_pairs = P.max_tile_pairs;
     A.stages = P.stages;
     A.stage_bytes = P.stage_bytes;

@@ -87,6 +87,7 @@ struct WinArgs {
     int32_t stages;             // TMA pipeline depth
     int32_t stage_bytes;
     int32_t rotate;             // batch-order rotation period (0/1: none)
+    int32_t combine;            // ring-free: combine equal-target scatters within a warp
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -399,6 +400,12 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
             // batches, so rows sharing their column lists (3x3 dof blocks) do not
             // hit the same scatter targets at the same time
             const int32_t rot = A.rotate > 1 && nb > 1 ? (g % A.rotate) % nb : 0;
+            // scatter combining (A.combine, ring-free only): every row's slots rotated by
+            // -g (mod m), so in one instruction neighbouring rows r, r+1 visit slots s and
+            // s-1 -- the same target whenever their offsets differ by one (stencil
+            // families) -- and lanes with equal targets add into one red.global
+            const bool comb = !RINGS && A.combine;
+            const int32_t gm = comb && m > 0 ? g % m : 0;
             for (int32_t bi = 0; bi < nb; ++bi) {
                 const int32_t bt = bi + rot < nb ? bi + rot : bi + rot - nb;
                 int32_t mm[4], j[4];
@@ -406,6 +413,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     mm[u] = L == 1 ? bt + u * nb : 4 * bt + u;
+                    if (comb && mm[u] < m) mm[u] = mm[u] >= gm ? mm[u] - gm : mm[u] + m - gm;
                     j[u] = mm[u] < m ? lds_i(ja_b + 4u * mm[u]) : -1;
                 }
 #pragma unroll
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
                         yi = fma(lds_f(al_b + E * mm[u], T(0)), xv[u], yi);
                         val[u] = lds_f(au_b + E * mm[u], T(0)) * xi;
                         if (!RINGS) {
-                            red_add((j[u] < rs ? sp : out) + j[u], val[u]);
+                            if (!comb) red_add((j[u] < rs ? sp : out) + j[u], val[u]);
                             continue;
                         }
                         const int32_t d = g - j[u];
@@ -432,7 +440,28 @@ __global__ void __launch_bounds__(32 + TR * L) k_windowed(WinArgs<T> A) {
                             red_add(out + j[u], val[u]);
                     }
                 }
-                if (!RINGS) continue;
+                if (!RINGS) {
+                    if (comb) {
+                        const unsigned am = __activemask();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const unsigned grp = __match_any_sync(am, j[u]);
+                            const int cnt = __popc(grp);
+                            const int mx = __reduce_max_sync(am, cnt);
+                            T tot = T(0);
+                            unsigned rest = grp;
+                            for (int k = 0; k < mx; ++k) {  // the k-th member's value, lane order
+                                const int src = rest ? __ffs(rest) - 1 : lane;
+                                const T o = __shfl_sync(am, val[u], src);
+                                if (rest) tot += o;
+                                rest &= rest - 1u;
+                            }
+                            if (j[u] >= 0 && lane == __ffs(grp) - 1)
+                                red_add((j[u] < rs ? sp : out) + j[u], tot);
+                        }
+                    }
+                    continue;
+                }
                 if (L == 1) {
                     T old[4];  // four independent CAS in flight
 #pragma unroll
