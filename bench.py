@@ -450,9 +450,24 @@ def run_multi(args, P, torch, world, rank, local, share):
     primary = "windowed" if args.kind == "windowed" else "gather"
     forms = {}
     clocks = None
+    use_abi = args.exec == "abi" and not share  # NCCL refuses two ranks on one GPU
     for form in [primary] + [f for f in ("gather", "windowed") if f != primary]:
-        ds = DistSpmv(a, P.Strategy(P.StrategyKind[form], dtype=dtype, device=local))
-        p = ds.plan
+        abi_err = None
+        if use_abi:
+            # the C-ABI executor: band plan + exchange lists + NCCL communicator in the library
+            from paper_1003_0952_b200.dist import NcclBandSpmv, gather_plan, halo_plan
+            try:
+                ds = NcclBandSpmv(a, P.Strategy(P.StrategyKind[form], dtype=dtype, device=local), form=form)
+                p = gather_plan(a, world, rank) if form == "gather" else halo_plan(a, world, rank)
+                L = ds.lists
+                assert (L.x_lo, L.x_hi, L.y_lo) == (p.x_lo, p.x_hi, p.y_lo)
+            except Exception as e:  # noqa: BLE001 -- reported in the JSON line, torch executor instead
+                abi_err = str(e)
+                ds = DistSpmv(a, P.Strategy(P.StrategyKind[form], dtype=dtype, device=local))
+                p = ds.plan
+        else:
+            ds = DistSpmv(a, P.Strategy(P.StrategyKind[form], dtype=dtype, device=local))
+            p = ds.plan
         xd = torch.from_numpy(x[p.x_lo:p.x_hi].copy()).to(device="cuda", dtype=tdt)
         yd = torch.zeros(p.row_end - p.y_lo, device="cuda", dtype=tdt)
         refresh = form == "gather"
@@ -493,7 +508,9 @@ def run_multi(args, P, torch, world, rank, local, share):
         dist.all_reduce(hb)
         halo = (sum(q1 - q0 for _, q0, q1 in p.x_sends) + sum(q1 - q0 for _, q0, q1 in p.x_recvs) if refresh else
                 sum(q1 - q0 for _, q0, q1 in p.sends) + sum(q1 - q0 for _, q0, q1 in p.recvs))
-        forms[form] = dict(ms_per_step=ms, gflops=flops / (ms / 1e3) / 1e9, effective_gbs=mb / (ms / 1e3) / 1e9,
+        forms[form] = dict(executor="C-ABI csrc_gpu_band_exec (NCCL in the library)" if use_abi and not abi_err
+                           else "paper_1003_0952_b200.dist.DistSpmv (torch.distributed)", abi_error=abi_err,
+                           ms_per_step=ms, gflops=flops / (ms / 1e3) / 1e9, effective_gbs=mb / (ms / 1e3) / 1e9,
                            e2e_ms=float(te.item()) * 1e3, e2e_gflops=flops / float(te.item()) / 1e9,
                            h2d_bytes_per_step=int(hb[0].item()), d2h_bytes_per_step=int(hb[1].item()),
                            exchange=("x halo (grouped NCCL send/recv), interior rows overlapped" if refresh else
@@ -534,6 +551,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=20.0, help="CPU-reference sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="cpu_baseline sample budget")
+    ap.add_argument("--exec", default="abi", choices=["abi", "torch"],
+                    help="N > 1: the C-ABI band executor (NCCL owned by the library) or the torch.distributed one")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -340,6 +340,52 @@ int csrc_colorful_slices(const csrc_host_matrix* a, const int32_t* color, int32_
 int64_t csrc_model_bytes(int64_t n, int64_t nnz_stored, int32_t value_symmetric, int32_t dtype);
 int64_t csrc_model_flops(int64_t n, int64_t nnz_full);
 
+/* ------------------------------------------------ multi-GPU band executor
+ * One per rank (one process per GPU). Rank g owns rows [b_g, b_{g+1}) of
+ * partition_by_nnz(a, world) (partition.hpp:55-90); every product includes the
+ * band form's exchange over NCCL (grouped ncclSend / ncclRecv on the executor's
+ * communication stream, overlapped with interior rows):
+ *   CSRC_BAND_WINDOWED  y halo: boundary rows' partials for [lo_g, b_g)
+ *                       (effective_range, partition.hpp:94-102) go to their
+ *                       owners, which add them -- the `effective` accumulation
+ *                       (parallel.hpp:371-382) at GPU granularity;
+ *   CSRC_BAND_GATHER    x halo (flags bit 0 = refresh): the owned x rows other
+ *                       bands read go to them before the boundary rows run.
+ * Device vectors: x covers [x_lo, x_hi), y covers [y_lo, row_end) (the lists).
+ * NCCL is loaded at run time (libnccl.so.2); the communicator's async errors
+ * are polled around every product and by csrc_gpu_band_exec_check. */
+enum { CSRC_BAND_WINDOWED = 0, CSRC_BAND_GATHER = 1 };
+
+typedef struct {
+    int32_t row_begin, row_end; /* owned rows                                   */
+    int32_t lo;                 /* effective_range lo of the owned rows          */
+    int32_t x_lo, x_hi;         /* the band's x range                            */
+    int32_t y_lo;               /* the band's y vector starts here               */
+    int32_t n_sends, n_recvs;   /* exchange messages per product                 */
+} csrc_gpu_band_lists;
+
+typedef struct csrc_gpu_band_exec_s* csrc_gpu_band_exec_t;
+
+/* ncclGetUniqueId on one rank (id: 128 bytes); the caller broadcasts it. */
+int csrc_gpu_nccl_get_unique_id(uint8_t* id);
+
+/* The exchange lists of rank `rank` (host only, no NCCL): sizes in *lists;
+ * arrays of n_sends / n_recvs entries (peer, [q0, q1) global rows), or NULL. */
+int csrc_gpu_band_lists_get(const csrc_host_matrix* a, int32_t world, int32_t rank, int32_t form,
+                            csrc_gpu_band_lists* lists, int32_t* send_peer, int32_t* send_q0, int32_t* send_q1,
+                            int32_t* recv_peer, int32_t* recv_q0, int32_t* recv_q1);
+
+int csrc_gpu_band_exec_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t world, int32_t rank,
+                              int32_t form, const uint8_t* nccl_id, csrc_gpu_band_exec_t* out);
+int csrc_gpu_band_exec_get_info(csrc_gpu_band_exec_t ex, csrc_gpu_band_lists* lists);
+/* the band plan the executor runs (owned by the executor) */
+int csrc_gpu_band_exec_plan(csrc_gpu_band_exec_t ex, csrc_gpu_plan_t* plan);
+/* y = A x on the band, exchange included, enqueued on `stream` (NULL: legacy stream). */
+int csrc_gpu_band_exec_apply(csrc_gpu_band_exec_t ex, const void* d_x, void* d_y, void* stream, int32_t flags);
+/* ncclCommGetAsyncError: nonzero (and the communicator aborted) after a failure. */
+int csrc_gpu_band_exec_check(csrc_gpu_band_exec_t ex);
+void csrc_gpu_band_exec_destroy(csrc_gpu_band_exec_t ex);
+
 /* ------------------------------------------------ CSRC construction
  * Device re-implementations of the reference's construction pipeline
  * (paper_1003_0952_b200/csrc/assemble.cu). Results are host arrays owned by

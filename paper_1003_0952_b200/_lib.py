@@ -126,6 +126,21 @@ plan_create_rect = _sig("csrc_gpu_plan_create_rect", C.c_int, PM, PS, i32, P_i32
                         C.POINTER(vp))
 plan_create_rect_plan = _sig("csrc_gpu_plan_create_rect_plan", C.c_int, PM, PS, i32, P_i32, P_i32, P_f64,
                              P_i32, i32, P_i32, i32, C.POINTER(vp))
+class BandLists(C.Structure):
+    _fields_ = [("row_begin", i32), ("row_end", i32), ("lo", i32), ("x_lo", i32), ("x_hi", i32), ("y_lo", i32),
+                ("n_sends", i32), ("n_recvs", i32)]
+
+
+nccl_get_unique_id = _sig("csrc_gpu_nccl_get_unique_id", C.c_int, C.POINTER(C.c_uint8))
+band_lists_get = _sig("csrc_gpu_band_lists_get", C.c_int, PM, i32, i32, i32, C.POINTER(BandLists),
+                      P_i32, P_i32, P_i32, P_i32, P_i32, P_i32)
+band_exec_create = _sig("csrc_gpu_band_exec_create", C.c_int, PM, PS, i32, i32, i32, C.POINTER(C.c_uint8),
+                        C.POINTER(vp))
+band_exec_get_info = _sig("csrc_gpu_band_exec_get_info", C.c_int, vp, C.POINTER(BandLists))
+band_exec_plan = _sig("csrc_gpu_band_exec_plan", C.c_int, vp, C.POINTER(vp))
+band_exec_apply = _sig("csrc_gpu_band_exec_apply", C.c_int, vp, vp, vp, vp, i32)
+band_exec_check = _sig("csrc_gpu_band_exec_check", C.c_int, vp)
+band_exec_destroy = _sig("csrc_gpu_band_exec_destroy", None, vp)
 bands_x_hi = _sig("csrc_bands_x_hi", C.c_int, PM, i32, P_i32, P_i32)
 plan_get_coloring = _sig("csrc_gpu_plan_get_coloring", C.c_int, vp, P_i32, P_i32)
 spmv_oneshot = _sig("csrc_gpu_spmv_oneshot", C.c_int, PM, P_f64, i64, P_f64, i32, i32)
@@ -185,6 +200,9 @@ EXPORTED = [
     "csrc_gpu_plan_create", "csrc_gpu_plan_create_colored", "csrc_gpu_plan_create_partitioned",
     "csrc_gpu_plan_create_band", "csrc_gpu_plan_create_rect", "csrc_gpu_plan_create_csr", "csrc_gpu_plan_destroy", "csrc_gpu_plan_get_info",
     "csrc_gpu_plan_create_rect_plan", "csrc_gpu_plan_get_coloring", "csrc_gpu_spmv_oneshot", "csrc_bands_x_hi",
+    "csrc_gpu_nccl_get_unique_id", "csrc_gpu_band_lists_get", "csrc_gpu_band_exec_create",
+    "csrc_gpu_band_exec_get_info", "csrc_gpu_band_exec_plan", "csrc_gpu_band_exec_apply", "csrc_gpu_band_exec_check",
+    "csrc_gpu_band_exec_destroy",
     "csrc_gpu_spmv", "csrc_gpu_spmv_transpose", "csrc_gpu_spmv_device",
     "csrc_gpu_spmv_device_graph", "csrc_gpu_halo_accumulate", "csrc_gpu_band_split",
     "csrc_gpu_gather_interior", "csrc_gpu_spmv_device_rows",

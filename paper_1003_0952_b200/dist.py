@@ -339,3 +339,72 @@ def gather_product(plan: HaloPlan, y_local, world_y: Optional[np.ndarray] = None
     if world_y is not None:
         world_y[plan.row_begin:plan.row_end] = own
     return own
+
+
+# ------------------------------------------------------------- C-ABI executor
+FORMS = {"windowed": 0, "gather": 1}
+
+
+def band_lists(a: CsrcMatrix, world: int, rank: int, form: str):
+    """The C-ABI executor's exchange lists (csrc_gpu_band_lists_get): (info,
+    sends [(peer, q0, q1)], recvs [(peer, q0, q1)])."""
+    import ctypes as C
+    from . import _check
+    from . import _lib as L
+    info = L.BandLists()
+    _check(L.band_lists_get(C.byref(a._c()), world, rank, FORMS[form], C.byref(info), None, None, None, None,
+                            None, None))
+    arr = [np.zeros(max(info.n_sends if i < 3 else info.n_recvs, 1), np.int32) for i in range(6)]
+    _check(L.band_lists_get(C.byref(a._c()), world, rank, FORMS[form], C.byref(info),
+                            *[x.ctypes.data_as(L.P_i32) for x in arr]))
+    sends = [(int(p), int(q0), int(q1)) for p, q0, q1 in zip(arr[0][:info.n_sends], arr[1], arr[2])]
+    recvs = [(int(p), int(q0), int(q1)) for p, q0, q1 in zip(arr[3][:info.n_recvs], arr[4], arr[5])]
+    return info, sends, recvs
+
+
+class NcclBandSpmv:
+    """The C-ABI band executor (csrc_gpu_band_exec_*, paper_1003_0952_b200/csrc/
+    bandexec.cpp): the band plan, the exchange lists and an NCCL communicator
+    owned by the product library. The NCCL unique id is created on rank 0 and
+    broadcast over the caller's torch.distributed group (any channel works)."""
+
+    def __init__(self, a: CsrcMatrix, strategy: Optional[Strategy] = None, form: str = "windowed", group=None):
+        import ctypes as C
+        import torch
+        import torch.distributed as dist
+        from . import _check
+        from . import _lib as L
+        self._L, self._check = L, _check
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        idb = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(L.nccl_get_unique_id(idb))
+        t = torch.tensor(list(bytes(idb)), dtype=torch.uint8)
+        if world > 1:
+            dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+            t = t.to(dev)
+            dist.broadcast(t, 0, group)
+            t = t.cpu()
+        idb = (C.c_uint8 * 128)(*t.tolist())
+        s = strategy or Strategy(StrategyKind[form])
+        self._h = C.c_void_p()
+        _check(L.band_exec_create(C.byref(a._c()), C.byref(s._c()), world, rank, FORMS[form], idb,
+                                  C.byref(self._h)))
+        info = L.BandLists()
+        _check(L.band_exec_get_info(self._h, C.byref(info)))
+        self.lists = info
+        self.form = form
+
+    def apply_device(self, x_local, y_local, refresh_x: bool = False, stream=None):
+        import torch
+        st = stream if stream is not None else torch.cuda.current_stream(x_local.device)
+        self._check(self._L.band_exec_apply(self._h, x_local.data_ptr(), y_local.data_ptr(),
+                                            int(st.cuda_stream) or None, 1 if refresh_x else 0))
+
+    def check(self):
+        self._check(self._L.band_exec_check(self._h))
+
+    def close(self):
+        if self._h:
+            self._L.band_exec_destroy(self._h)
+            self._h = None

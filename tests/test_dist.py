@@ -164,3 +164,21 @@ def test_bands_x_hi_matches_the_numpy_definition():
         for p in (1, 2, 3, 8, 16):
             bs = P.partition_by_nnz(a, p).block_start
             assert bands_x_hi(a, bs) == [band_x_hi(a, bs[b], bs[b + 1]) for b in range(p)]
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_c_abi_exchange_lists_match_the_python_plans(cfg):
+    """The C-ABI band executor (csrc/bandexec.cpp) derives the same exchange
+    lists as paper_1003_0952_b200.dist (halo_plan / gather_plan)."""
+    from paper_1003_0952_b200.dist import band_lists, gather_plan, halo_plan
+    a, _, _ = P.config_matrix(cfg)
+    for world in (1, 2, 3, 5, 8):
+        for rank in range(world):
+            info, sends, recvs = band_lists(a, world, rank, "windowed")
+            h = halo_plan(a, world, rank)
+            assert (sends, recvs) == (h.sends, h.recvs)
+            assert (info.row_begin, info.row_end, info.lo, info.y_lo) == (h.row_begin, h.row_end, h.lo, h.lo)
+            info, sends, recvs = band_lists(a, world, rank, "gather")
+            g = gather_plan(a, world, rank)
+            assert sorted(sends) == sorted(g.x_sends) and sorted(recvs) == sorted(g.x_recvs)
+            assert (info.x_lo, info.x_hi, info.y_lo) == (g.x_lo, g.x_hi, g.y_lo)
