@@ -36,7 +36,7 @@ struct Error : std::runtime_error {
 };
 thread_local std::string g_fixture_error;
 template <class F>
-int guarded(F&& f) {
+int guarded(const char*, F&& f) {
     try {
         f();
         return 0;
@@ -336,7 +336,7 @@ using namespace csrcgpu;
 extern "C" {
 
 int csrc_fixture_generate(const csrc_fixture_spec* spec, csrc_fixture_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!spec || !out) throw Error("csrc_fixture_generate: null argument");
         *out = nullptr;
         auto fx = std::make_unique<csrc_fixture_s>();
@@ -346,7 +346,7 @@ int csrc_fixture_generate(const csrc_fixture_spec* spec, csrc_fixture_t* out) {
 }
 
 int csrc_fixture_matrix(csrc_fixture_t fx, csrc_host_matrix* m) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!fx || !m) throw Error("csrc_fixture_matrix: null argument");
         m->n = fx->n;
         m->k = static_cast<int64_t>(fx->ja.size());

@@ -460,7 +460,7 @@ extern "C" {
 
 int csrc_gpu_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t* rows,
                        const int32_t* cols, const double* vals, int32_t device, csrc_built_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("build_csr: null output handle");
         *out = nullptr;
         if (n_rows < 0 || n_cols < 0) throw Error("build_csr: negative dimensions");
@@ -490,7 +490,7 @@ int csrc_gpu_build_csr(int32_t n_rows, int32_t n_cols, int64_t m, const int32_t*
 
 int csrc_gpu_build_csrc(int32_t n, int64_t m, const int32_t* rows, const int32_t* cols,
                         const double* vals, int32_t device, csrc_built_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("build_csr: null output handle");
         *out = nullptr;
         if (n < 0) throw Error("build_csr: negative dimensions");
@@ -519,7 +519,7 @@ int csrc_gpu_build_csrc(int32_t n, int64_t m, const int32_t* rows, const int32_t
 int csrc_gpu_csr_to_csrc(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
                          const int32_t* col_idx, const double* values, int32_t device,
                          csrc_built_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("csr_to_csrc: null output handle");
         *out = nullptr;
         if (n_rows != n_cols) throw Error("csr_to_csrc: matrix is not square");
@@ -552,7 +552,7 @@ int csrc_gpu_csr_to_csrc(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
 int csrc_gpu_decompose_rect(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr,
                             const int32_t* col_idx, const double* values, int32_t device,
                             csrc_built_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("decompose_rect: null output handle");
         *out = nullptr;
         if (n_cols <= n_rows)
@@ -595,7 +595,7 @@ int csrc_gpu_decompose_rect(int32_t n_rows, int32_t n_cols, const int32_t* row_p
 }
 
 int csrc_built_matrix(csrc_built_t b, csrc_host_matrix* m) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!b || !m) throw Error("csrc_built_matrix: null argument");
         if (!b->has_csrc) throw Error("csrc_built_matrix: handle holds no CSRC matrix");
         m->n = b->n;
@@ -611,7 +611,7 @@ int csrc_built_matrix(csrc_built_t b, csrc_host_matrix* m) {
 
 int csrc_built_csr(csrc_built_t b, int32_t* n_rows, int32_t* n_cols, int64_t* nnz,
                    const int32_t** row_ptr, const int32_t** col_idx, const double** values) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!b) throw Error("csrc_built_csr: null handle");
         if (!b->has_csr) throw Error("csrc_built_csr: handle holds no CSR matrix");
         *n_rows = b->n_rows;
@@ -625,7 +625,7 @@ int csrc_built_csr(csrc_built_t b, int32_t* n_rows, int32_t* n_cols, int64_t* nn
 
 int csrc_built_rect_tail(csrc_built_t b, int32_t* m_cols, int64_t* nnz, const int32_t** row_ptr,
                          const int32_t** col_idx, const double** values) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!b) throw Error("csrc_built_rect_tail: null handle");
         if (!b->has_rect) throw Error("csrc_built_rect_tail: handle holds no rectangular tail");
         *m_cols = b->m_cols;
@@ -637,7 +637,7 @@ int csrc_built_rect_tail(csrc_built_t b, int32_t* m_cols, int64_t* nnz, const in
 }
 
 int csrc_built_timings(csrc_built_t b, double* ms4) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!b || !ms4) throw Error("csrc_built_timings: null argument");
         for (int q = 0; q < 4; ++q) ms4[q] = b->ms[q];
     });

@@ -209,7 +209,7 @@ void grouped(F&& f) {
 extern "C" {
 
 int csrc_gpu_nccl_get_unique_id(uint8_t* id) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!id) throw Error("null id");
         ncclUniqueId u;
         nccl_ok(nccl().getUniqueId(&u), "ncclGetUniqueId");
@@ -220,7 +220,7 @@ int csrc_gpu_nccl_get_unique_id(uint8_t* id) {
 int csrc_gpu_band_lists_get(const csrc_host_matrix* a, int32_t world, int32_t rank, int32_t form,
                             csrc_gpu_band_lists* lists, int32_t* send_peer, int32_t* send_q0, int32_t* send_q1,
                             int32_t* recv_peer, int32_t* recv_q0, int32_t* recv_q1) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!a || !lists) throw Error("null argument");
         if (world < 1 || rank < 0 || rank >= world) throw Error("band lists: need 0 <= rank < world");
         std::vector<int32_t> sp, s0, s1, rp, r0, r1;
@@ -239,7 +239,7 @@ int csrc_gpu_band_lists_get(const csrc_host_matrix* a, int32_t world, int32_t ra
 
 int csrc_gpu_band_exec_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t world, int32_t rank,
                               int32_t form, const uint8_t* id, csrc_gpu_band_exec_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!a || !s || !id || !out) throw Error("null argument");
         *out = nullptr;
         if (world < 1 || rank < 0 || rank >= world) throw Error("band executor: need 0 <= rank < world");
@@ -280,21 +280,21 @@ int csrc_gpu_band_exec_create(const csrc_host_matrix* a, const csrc_gpu_strategy
 }
 
 int csrc_gpu_band_exec_get_info(csrc_gpu_band_exec_t ex, csrc_gpu_band_lists* lists) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ex || !lists) throw Error("null argument");
         *lists = ex->lists;
     });
 }
 
 int csrc_gpu_band_exec_plan(csrc_gpu_band_exec_t ex, csrc_gpu_plan_t* plan) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ex || !plan) throw Error("null argument");
         *plan = ex->plan;
     });
 }
 
 int csrc_gpu_band_exec_apply(csrc_gpu_band_exec_t ex, const void* d_x, void* d_y, void* stream, int32_t flags) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ex) throw Error("null executor");
         ex->poll();
         BX_CUDA(cudaSetDevice(ex->device));
@@ -369,7 +369,7 @@ int csrc_gpu_band_exec_apply(csrc_gpu_band_exec_t ex, const void* d_x, void* d_y
 }
 
 int csrc_gpu_band_exec_check(csrc_gpu_band_exec_t ex) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!ex) throw Error("null executor");
         ex->poll();
     });

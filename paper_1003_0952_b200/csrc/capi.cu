@@ -2538,7 +2538,7 @@ int csrc_gpu_device_count(void) {
 
 int csrc_gpu_plan_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                          csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("null output");
         *out = nullptr;
         *out = create_plan(a, s, CreateOpts{});
@@ -2547,7 +2547,7 @@ int csrc_gpu_plan_create(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
 
 int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                                  const int32_t* color, int32_t n_colors, csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out || !color) throw Error("null argument");
         *out = nullptr;
         CreateOpts o;
@@ -2559,7 +2559,7 @@ int csrc_gpu_plan_create_colored(const csrc_host_matrix* a, const csrc_gpu_strat
 
 int csrc_gpu_plan_create_csr(int32_t n_rows, int32_t n_cols, const int32_t* row_ptr, const int32_t* col_idx,
                              const double* values, const csrc_gpu_strategy* s, csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("null output");
         *out = nullptr;
         *out = create_csr_plan(n_rows, n_cols, row_ptr, col_idx, values, s);
@@ -2569,7 +2569,7 @@ int csrc_gpu_plan_create_csr(int32_t n_rows, int32_t n_cols, const int32_t* row_
 int csrc_gpu_plan_create_rect(const csrc_host_matrix* a, const csrc_gpu_strategy* s, int32_t m_cols,
                               const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
                               const double* tail_values, csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("null output");
         *out = nullptr;
         CreateOpts o;
@@ -2586,7 +2586,7 @@ int csrc_gpu_plan_create_rect_plan(const csrc_host_matrix* a, const csrc_gpu_str
                                    const int32_t* tail_row_ptr, const int32_t* tail_col_idx,
                                    const double* tail_values, const int32_t* color, int32_t n_colors,
                                    const int32_t* block_start, int32_t bands, csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("null output");
         *out = nullptr;
         if ((color != nullptr) == (block_start != nullptr))
@@ -2606,7 +2606,7 @@ int csrc_gpu_plan_create_rect_plan(const csrc_host_matrix* a, const csrc_gpu_str
 }
 
 int csrc_gpu_plan_get_coloring(csrc_gpu_plan_t plan, int32_t* color, int32_t* n_colors) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (n_colors) *n_colors = P.n_colors;
         if (color && !P.host_color.empty())
@@ -2617,7 +2617,7 @@ int csrc_gpu_plan_get_coloring(csrc_gpu_plan_t plan, int32_t* color, int32_t* n_
 int csrc_gpu_plan_create_partitioned(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                                      const int32_t* block_start, int32_t bands,
                                      csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out || !block_start) throw Error("null argument");
         *out = nullptr;
         CreateOpts o;
@@ -2629,7 +2629,7 @@ int csrc_gpu_plan_create_partitioned(const csrc_host_matrix* a, const csrc_gpu_s
 
 int csrc_gpu_plan_create_band(const csrc_host_matrix* a, const csrc_gpu_strategy* s,
                               int32_t row_begin, int32_t row_end, csrc_gpu_plan_t* out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         if (!out) throw Error("null output");
         *out = nullptr;
         CreateOpts o;
@@ -2649,7 +2649,7 @@ void csrc_gpu_plan_destroy(csrc_gpu_plan_t plan) {
 }
 
 int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (!info) throw Error("null info");
         std::memset(info, 0, sizeof(*info));
@@ -2729,12 +2729,12 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
 }
 
 int csrc_gpu_spmv(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, double* y_host) {
-    return guarded([&] { apply_host(*checked(plan), x_host, x_len, y_host, false); });
+    return guarded(__func__, [&] { apply_host(*checked(plan), x_host, x_len, y_host, false); });
 }
 
 int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len,
                             double* y_host) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (P.m_cols) throw Error("spmv_csrc_transpose: rectangular plans have no transpose product");
         if (P.is_csr) throw Error("spmv_csr: CSR plans have no transpose product");
@@ -2747,7 +2747,7 @@ int csrc_gpu_spmv_transpose(csrc_gpu_plan_t plan, const double* x_host, int64_t 
 
 int csrc_gpu_spmv_device(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream,
                          int32_t flags) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
         apply_device(P, d_x, d_y, st, (flags & 1) && !P.value_symmetric);
@@ -2755,7 +2755,7 @@ int csrc_gpu_spmv_device(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void*
 }
 
 int csrc_gpu_spmv_device_graph(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
         CUDA_OK(cudaSetDevice(P.device));
@@ -2787,7 +2787,7 @@ int csrc_gpu_spmv_device_graph(csrc_gpu_plan_t plan, const void* d_x, void* d_y,
 
 int csrc_gpu_halo_accumulate(csrc_gpu_plan_t plan, void* d_y, int64_t dst_off,
                              const void* d_recv, int64_t len, void* stream) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (len <= 0) return;
         cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : P.stream;
@@ -2803,7 +2803,7 @@ int csrc_gpu_halo_accumulate(csrc_gpu_plan_t plan, void* d_y, int64_t dst_off,
 }
 
 int csrc_gpu_gather_interior(csrc_gpu_plan_t plan, int32_t* rows_begin, int32_t* rows_end) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (P.exec_kind != CSRC_KIND_GATHER) throw Error("interior rows are defined for gather plans");
         *rows_begin = P.gi0;
@@ -2813,7 +2813,7 @@ int csrc_gpu_gather_interior(csrc_gpu_plan_t plan, int32_t* rows_begin, int32_t*
 
 int csrc_gpu_spmv_device_rows(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream, int32_t flags,
                               int32_t rows_begin, int32_t rows_end) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (P.exec_kind != CSRC_KIND_GATHER) throw Error("row-range products need a gather plan");
         if (P.m_cols) throw Error("row-range products need a square plan");
@@ -2837,7 +2837,7 @@ int csrc_gpu_spmv_device_rows(csrc_gpu_plan_t plan, const void* d_x, void* d_y, 
 }
 
 int csrc_gpu_band_split(csrc_gpu_plan_t plan, int32_t* boundary_rows_end) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         *boundary_rows_end = P.split;
     });
@@ -2845,7 +2845,7 @@ int csrc_gpu_band_split(csrc_gpu_plan_t plan, int32_t* boundary_rows_end) {
 
 int csrc_gpu_spmv_device_part(csrc_gpu_plan_t plan, const void* d_x, void* d_y, void* stream,
                               int32_t part) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (part != 0 && part != 1) throw Error("part must be 0 (boundary) or 1 (interior)");
         if (P.row_begin == 0 && P.row_end == P.n_global)
@@ -2858,11 +2858,11 @@ int csrc_gpu_spmv_device_part(csrc_gpu_plan_t plan, const void* d_x, void* d_y, 
 }
 
 int csrc_gpu_set_timing(csrc_gpu_plan_t plan, int32_t enabled) {
-    return guarded([&] { checked(plan)->timing = enabled != 0; });
+    return guarded(__func__, [&] { checked(plan)->timing = enabled != 0; });
 }
 
 int csrc_gpu_last_timings(csrc_gpu_plan_t plan, csrc_gpu_timings* t) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         std::memset(t, 0, sizeof(*t));
         if (!P.ev_recorded) return;
@@ -2879,7 +2879,7 @@ int csrc_gpu_last_timings(csrc_gpu_plan_t plan, csrc_gpu_timings* t) {
 
 int csrc_gpu_time_products(csrc_gpu_plan_t plan, const void* d_x, void* d_y, int32_t reps,
                            int64_t flush_bytes, double* ms_out, double* kernel_ms_out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (reps < 1) throw Error("reps must be >= 1");
         CUDA_OK(cudaSetDevice(P.device));
@@ -2911,7 +2911,7 @@ int csrc_gpu_time_products(csrc_gpu_plan_t plan, const void* d_x, void* d_y, int
 
 int csrc_gpu_time_products_host(csrc_gpu_plan_t plan, const double* x_host, int64_t x_len, int32_t reps,
                                 int64_t flush_bytes, double* ms_out, double* kernel_ms_out) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Plan& P = *checked(plan);
         if (x_len != P.x_len())
             throw Error("ParallelSpmv: x has length " + std::to_string(x_len) + ", expected " +

@@ -6,6 +6,11 @@
 #include <string>
 #include <vector>
 
+#if __has_include(<nvtx3/nvToolsExt.h>)
+#include <nvtx3/nvToolsExt.h>
+#define CSRC_GPU_NVTX 1
+#endif
+
 #include "../../include/csrc_gpu.h"
 
 namespace csrcgpu {
@@ -21,8 +26,24 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg);
 
+// NVTX range over one C-ABI call (header-only NVTX3: a no-op unless a tool such
+// as nsys/ncu injects itself; `ncu --nvtx --nvtx-include csrc_gpu_spmv/` filters
+// the launches of one entry point). Plan builds, host products, band exchanges
+// and construction calls show up by their ABI names on a timeline.
+struct NvtxRange {
+#ifdef CSRC_GPU_NVTX
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+#else  // a translation unit built without the CUDA headers (the standalone fixture library)
+    explicit NvtxRange(const char*) {}
+#endif
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 template <class F>
-int guarded(F&& f) {
+int guarded(const char* entry, F&& f) {
+    NvtxRange range(entry);
     try {
         f();
         return 0;

@@ -242,7 +242,7 @@ void run(const MatView& a, const double* xh, double* yh, bool transpose, int dev
 
 extern "C" int csrc_gpu_spmv_oneshot(const csrc_host_matrix* m, const double* x_host, int64_t x_len,
                                      double* y_host, int32_t transpose, int32_t device) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         Trace tr;
         MatView a = view_of(m, true);
         tr.mark("structure check");

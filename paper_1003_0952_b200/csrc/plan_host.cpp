@@ -402,7 +402,7 @@ int csrc_gpu_abi_version(void) { return CSRC_GPU_ABI_VERSION; }
 
 int csrc_partition_by_nnz(const csrc_host_matrix* m, int32_t p, int32_t* block_start,
                           int64_t* block_nnz) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         RowPartition part = partition_by_nnz(a, p);
         if (block_start) std::copy(part.block_start.begin(), part.block_start.end(), block_start);
@@ -412,7 +412,7 @@ int csrc_partition_by_nnz(const csrc_host_matrix* m, int32_t p, int32_t* block_s
 
 int csrc_effective_ranges(const csrc_host_matrix* m, int32_t p, const int32_t* block_start,
                           int32_t* lo, int32_t* hi) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         if (p < 1) throw Error("effective_ranges: p must be >= 1");
         std::vector<index_t> bs(block_start, block_start + p + 1), l, h;
@@ -423,7 +423,7 @@ int csrc_effective_ranges(const csrc_host_matrix* m, int32_t p, const int32_t* b
 }
 
 int csrc_bands_x_hi(const csrc_host_matrix* m, int32_t p, const int32_t* block_start, int32_t* x_hi) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         if (p < 1) throw Error("bands_x_hi: p must be >= 1");
         // x_hi[b] = max(row_end_b, 1 + the last row whose lower columns fall in band b);
@@ -465,7 +465,7 @@ int csrc_interval_plan(int32_t p, const int32_t* lo, const int32_t* hi, int32_t*
                        int32_t* n_contrib, int32_t* n_boundaries, int32_t* iv_begin,
                        int32_t* iv_end, int32_t* contrib_ptr, int32_t* contrib,
                        int32_t* boundaries) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         std::vector<index_t> l(lo, lo + p), h(hi, hi + p);
         IntervalPlan plan = build_interval_plan(l, h);
         *n_intervals = static_cast<int32_t>(plan.iv_begin.size());
@@ -481,7 +481,7 @@ int csrc_interval_plan(int32_t p, const int32_t* lo, const int32_t* hi, int32_t*
 
 int csrc_color_rows(const csrc_host_matrix* m, int32_t mode, int32_t order, int32_t* color,
                     int32_t* n_colors) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         int nc = 0;
         std::vector<int32_t> c = color_rows(a, mode, order, &nc);
@@ -492,7 +492,7 @@ int csrc_color_rows(const csrc_host_matrix* m, int32_t mode, int32_t order, int3
 
 int csrc_conflict_edge_counts(const csrc_host_matrix* m, int32_t mode, int64_t* n_direct,
                               int64_t* n_indirect) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         conflict_edge_counts(a, mode, n_direct, n_indirect);
     });
@@ -500,7 +500,7 @@ int csrc_conflict_edge_counts(const csrc_host_matrix* m, int32_t mode, int64_t* 
 
 int csrc_validate_coloring(const csrc_host_matrix* m, const int32_t* color, int32_t n_colors,
                            int32_t* valid, int32_t* row_a, int32_t* row_b, int32_t* position) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         Validity v = validate_coloring(a, color, n_colors);
         *valid = v.valid ? 1 : 0;
@@ -513,7 +513,7 @@ int csrc_validate_coloring(const csrc_host_matrix* m, const int32_t* color, int3
 // parallel.hpp:69-93 ColorfulPlan::slice
 int csrc_colorful_slices(const csrc_host_matrix* m, const int32_t* color, int32_t n_colors,
                          int32_t p, int64_t* slices) {
-    return guarded([&] {
+    return guarded(__func__, [&] {
         MatView a = view_of(m, false);
         if (p < 1) throw Error("colorful_slices: p must be >= 1");
         std::vector<std::vector<index_t>> classes(static_cast<size_t>(n_colors));
