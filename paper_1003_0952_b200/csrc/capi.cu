@@ -232,6 +232,10 @@ struct csrc_gpu_plan_s {
     int cw_pf = 1;
     int64_t cw_rows = 0, cw_block_rows = 0;
     DevBuf cw_tk, cw_nch, cw_ctr, cw_xp, cw_yp;
+    // ring form (k_colored_ring): pairs packed per sub-chunk, TMA-staged
+    bool cw_ring = false;
+    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0;
+    DevBuf cpk;
 
     // host-path scratch
     DevBuf dx, dy, dxd, dyd, flushbuf;
@@ -767,20 +771,48 @@ const void* colored_wave_fn(const Plan& P) {
 }
 
 template <class T>
+const void* colored_ring_fn(const Plan& P) {
+    if (P.cr_hint) {
+        switch (P.cw_u) {
+            case 16: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 16, true>);
+            case 14: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 14, true>);
+            case 4: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 4, true>);
+            default: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, true>);
+        }
+    }
+    switch (P.cw_u) {
+        case 16: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 16, false>);
+        case 14: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 14, false>);
+        case 4: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 4, false>);
+        default: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, false>);
+    }
+}
+
+template <class T>
 void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& color, int C) {
     const index_t n = a.n;
     count_t bw = 0;
     for (index_t i = 0; i < n; ++i)
         if (a.ia[i + 1] > a.ia[i]) bw = std::max<count_t>(bw, i - a.ja[a.ia[i]]);
     {
-        const int u = env_int("CSRC_GPU_CW_U", 8);
-        P.cw_u = (u == 4 || u == 16) ? u : 8;
+        P.cw_ring = env_int("CSRC_GPU_CW_RING", 1) != 0;
+        const int u = env_int("CSRC_GPU_CW_U", P.cw_ring ? 14 : 8);
+        P.cw_u = (u == 4 || u == 16 || (u == 14 && P.cw_ring)) ? u : 8;
         P.cw_nt = env_int("CSRC_GPU_CW_NT", 128) == 256 ? 256 : 128;
         P.cw_pf = env_int("CSRC_GPU_CW_PF", 1);
+        if (P.cw_ring) P.cw_nt = dev::kCrRows;
+        P.cr_stages = std::min(dev::kCrMaxStages, std::max(2, env_int("CSRC_GPU_CR_STAGES", 2)));
+        P.cr_hint = env_int("CSRC_GPU_CR_HINT", 0) != 0;
     }
+    const bool ring = P.cw_ring;
+    // ring form: bytes per stored pair, pairs per row a stage holds (one sub-chunk)
+    const int64_t pair_bytes = 4 + static_cast<int64_t>(sizeof(T)) * (a.value_symmetric ? 1 : 2);
+    const int ws_max = static_cast<int>(std::max<int64_t>(
+        1, static_cast<int64_t>(env_int("CSRC_GPU_CR_STAGE_BYTES", 33280)) / (dev::kCrRows * pair_bytes)));
+    P.cr_stage_bytes = static_cast<int>(ws_max * dev::kCrRows * pair_bytes);
     // blocks of B rows, R = ceil(bw / B): rows more than R blocks apart never write the
     // same y position (row i writes only on [i - bw, i])
-    const int r_target = std::max(1, env_int("CSRC_GPU_CW_R", 4));
+    const int r_target = std::min(15, std::max(1, env_int("CSRC_GPU_CW_R", 4)));
     const int64_t min_rows = env_int("CSRC_GPU_CW_MINB", 32) * static_cast<int64_t>(C);
     int64_t B = std::max<int64_t>({(bw + r_target - 1) / r_target, min_rows, 256});
     B = std::min<int64_t>(B, std::max<index_t>(n, 1));
@@ -826,7 +858,7 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
             if (e == 0 || e == NE - 1) {
                 r0 = start[static_cast<size_t>(b) * C];
                 r1 = start[static_cast<size_t>(b + 1) * C];
-                step = 1024;
+                step = ring ? dev::kCrCopy : 1024;
             } else {
                 r0 = start[static_cast<size_t>(b) * C + (e - 1)];
                 r1 = r0 + cnt[static_cast<size_t>(b) * C + (e - 1)];
@@ -843,7 +875,13 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
                     for (int64_t r = q; r < t.r1; ++r) w = std::max<int32_t>(w, a.ia[rid[r] + 1] - a.ia[rid[r]]);
                     t.w = w;
                     t.ebase = ne;
-                    ne += (static_cast<int64_t>(w) * NT + 3) / 4 * 4;
+                    if (ring) {  // ne counts bytes: sub-chunks of ws pairs per row, each [ja | al | au]
+                        const int nsub = std::max(1, (w + ws_max - 1) / ws_max);
+                        t.pad = w ? (w + nsub - 1) / nsub : 1;
+                        ne += static_cast<int64_t>(w) * NT * pair_bytes;
+                    } else {
+                        ne += (static_cast<int64_t>(w) * NT + 3) / 4 * 4;
+                    }
                 }
                 chunks[task].push_back(t);
             }
@@ -859,14 +897,57 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
             }
             nch[task] = static_cast<int32_t>(chunks[task].size());
         }
-    HVec<int32_t> cja(static_cast<size_t>(std::max<int64_t>(ne, 4)));
-    HVec<double> cal(static_cast<size_t>(std::max<int64_t>(ne, 4))), cau, cad(static_cast<size_t>(npad), 0.0);
-    if (!a.value_symmetric) cau = HVec<double>(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+    HVec<int32_t> cja;
+    HVec<double> cal, cau, cad(static_cast<size_t>(npad), 0.0);
+    HVec<unsigned char> cpk;
+    if (ring) {
+        cpk = HVec<unsigned char>(static_cast<size_t>(ne) + 16);
+    } else {
+        cja = HVec<int32_t>(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+        cal = HVec<double>(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+        if (!a.value_symmetric) cau = HVec<double>(static_cast<size_t>(std::max<int64_t>(ne, 4)));
+    }
     for (int64_t r = 0; r < npad; ++r) cad[r] = rid[r] >= 0 ? a.ad[rid[r]] : 0.0;
     std::vector<const dev::CwTicket*> cls;
     for (auto& v : chunks)
         for (auto& t : v)
             if (t.e >= 1 && t.e <= C && t.w > 0) cls.push_back(&t);
+    if (ring) {
+        // sub-chunk k of a chunk (pairs [k ws, k ws + nq) of its rows): nq NT column ids,
+        // nq NT lower values, nq NT upper values, pair q of row l at slot q NT + l
+        parallel_slices(static_cast<int64_t>(cls.size()), [&](int, int64_t c0, int64_t c1) {
+            for (int64_t k = c0; k < c1; ++k) {
+                const dev::CwTicket& t = *cls[k];
+                const int ws = t.pad;
+                unsigned char* base = cpk.data() + t.ebase;
+                for (int32_t q0 = 0; q0 < t.w; q0 += ws) {
+                    const int32_t nq = std::min<int32_t>(ws, t.w - q0);
+                    int32_t* pj = reinterpret_cast<int32_t*>(base);
+                    T* pl = reinterpret_cast<T*>(base + static_cast<size_t>(nq) * NT * 4);
+                    T* pu = pl + static_cast<size_t>(nq) * NT;
+                    for (int32_t l = 0; l < NT; ++l) {
+                        const int64_t r = static_cast<int64_t>(t.r0) + l;
+                        const int32_t i = r < t.r1 ? rid[r] : -1;
+                        const int32_t len = i >= 0 ? a.ia[i + 1] - a.ia[i] : 0;
+                        for (int32_t q = 0; q < nq; ++q) {
+                            const size_t e = static_cast<size_t>(q) * NT + l;
+                            if (q0 + q < len) {
+                                const int64_t sidx = a.ia[i] + q0 + q;
+                                pj[e] = pos[a.ja[sidx]];
+                                pl[e] = static_cast<T>(a.al[sidx]);
+                                if (!a.value_symmetric) pu[e] = static_cast<T>(a.au[sidx]);
+                            } else {  // padding: own row, zero values (never gathered nor scattered)
+                                pj[e] = static_cast<int32_t>(r);
+                                pl[e] = T(0);
+                                if (!a.value_symmetric) pu[e] = T(0);
+                            }
+                        }
+                    }
+                    base += static_cast<size_t>(nq) * NT * pair_bytes;
+                }
+            }
+        }, 64);
+    } else {
     parallel_slices(static_cast<int64_t>(cls.size()), [&](int, int64_t c0, int64_t c1) {
         for (int64_t k = c0; k < c1; ++k) {
             const dev::CwTicket& t = *cls[k];
@@ -896,10 +977,26 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
             }
         }
     }, 64);
+    }
     // dispatch along diagonals b + D e (D > R): class e trails class e-1 by D blocks, so
     // (e, b)'s dependencies (e-1, b-R .. b+R) lie D - R diagonals earlier; all classes
-    // are in flight at once over a window of ~D (C + 2) blocks (x, y L2-resident)
-    const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", 4 * R));  // C5 1.72 ms vs 2.12 at 2R (profiles/r02_colored_wave_sweep.txt)
+    // are in flight at once over a window of ~D (C + 2) blocks (x, y L2-resident).
+    // D B must cover the bandwidth plus the rows whose read-add-write phase is in flight:
+    // every resident thread's row for the direct form (D = 4 R at C5: 1.72 ms vs 2.12 at
+    // 2 R, profiles/r02_colored_wave_sweep.txt), only the consumer rows of the ring form.
+    const void* fn = ring ? colored_ring_fn<T>(P) : colored_wave_fn<T>(P);
+    const int smem = ring ? P.cr_stages * P.cr_stage_bytes : 0;
+    if (ring) set_smem_limit(fn, smem);
+    int occ = 0;
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ring ? dev::kCrThreads : P.cw_nt, smem));
+    const int per_sm = env_int("CSRC_GPU_CW_CTAS", std::max(occ, 1));
+    const int grid_max = num_sms(P.device) * std::min(per_sm, std::max(occ, 1));
+    int d_default = 4 * R;
+    if (ring) {
+        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", 200) / 100.0;
+        d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * dev::kCrRows) / static_cast<double>(B)));
+    }
+    const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", d_default));
     std::vector<int> order(P.cw_tasks);
     std::iota(order.begin(), order.end(), 0);
     auto key = [&](int t) {
@@ -911,22 +1008,22 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     for (int t : order)
         for (const dev::CwTicket& c : chunks[t]) tk.push_back(c);
     P.cw_tickets = static_cast<int>(tk.size());
-    const size_t ne_up = static_cast<size_t>(std::max<int64_t>(ne, 4));
     upload(P.rid, rid.data(), rid.size());
-    upload(P.cja, cja.data(), ne_up);
-    upload_values<T>(P.cal, cal.data(), ne_up);
-    if (!a.value_symmetric) upload_values<T>(P.cau, cau.data(), ne_up);
+    if (ring) {
+        upload(P.cpk, cpk.data(), static_cast<size_t>(ne) + 16);
+    } else {
+        const size_t ne_up = static_cast<size_t>(std::max<int64_t>(ne, 4));
+        upload(P.cja, cja.data(), ne_up);
+        upload_values<T>(P.cal, cal.data(), ne_up);
+        if (!a.value_symmetric) upload_values<T>(P.cau, cau.data(), ne_up);
+    }
     upload_values<T>(P.cad, cad.data(), static_cast<size_t>(npad));
     upload(P.cw_tk, tk.data(), tk.size());
     upload(P.cw_nch, nch.data(), nch.size());
     P.cw_ctr.alloc(static_cast<size_t>(P.cw_tasks + 1) * 4);
     P.cw_xp.alloc(static_cast<size_t>(npad) * sizeof(T));
     P.cw_yp.alloc(static_cast<size_t>(npad) * sizeof(T));
-    const void* fn = colored_wave_fn<T>(P);
-    int occ = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P.cw_nt, 0));
-    const int per_sm = env_int("CSRC_GPU_CW_CTAS", std::max(occ, 1));
-    P.cw_grid = std::max(1, std::min(P.cw_tickets, num_sms(P.device) * std::min(per_sm, std::max(occ, 1))));
+    P.cw_grid = std::max(1, std::min(P.cw_tickets, grid_max));
     P.cw = true;
 }
 
@@ -2061,7 +2158,40 @@ void launch_atomic(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
 }
 
 template <class T>
+void launch_colored_ring(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    dev::ColorRingArgs<T> A{};
+    A.tickets = P.cw_tk.as<dev::CwTicket>();
+    A.nch = P.cw_nch.as<int32_t>();
+    A.ctr = P.cw_ctr.as<int32_t>();
+    A.n_tickets = P.cw_tickets;
+    A.n_blocks = P.cw_blocks;
+    A.n_e = P.n_colors + 2;
+    A.radius = P.cw_radius;
+    A.rid = P.rid.as<int32_t>();
+    A.pk = P.cpk.as<unsigned char>();
+    A.ad = P.cad.as<T>();
+    A.x = x;
+    A.y = y;
+    A.xp = P.cw_xp.as<T>();
+    A.yp = P.cw_yp.as<T>();
+    A.stages = P.cr_stages;
+    A.stage_bytes = P.cr_stage_bytes;
+    A.sym = P.value_symmetric ? 1 : 0;
+    A.tr = tr ? 1 : 0;
+    CUDA_OK(cudaMemsetAsync(P.cw_ctr.p, 0, static_cast<size_t>(P.cw_tasks + 1) * 4, st));
+    const void* fn = colored_ring_fn<T>(P);
+    const int smem = P.cr_stages * P.cr_stage_bytes;
+    set_smem_limit(fn, smem);
+    void* args[] = {&A};
+    CUDA_OK(cudaLaunchKernel(fn, dim3(P.cw_grid), dim3(dev::kCrThreads), args, smem, st));
+}
+
+template <class T>
 void launch_colored_wave(const Plan& P, bool tr, const T* x, T* y, cudaStream_t st) {
+    if (P.cw_ring) {
+        launch_colored_ring<T>(P, tr, x, y, st);
+        return;
+    }
     dev::ColorWaveArgs<T> A{};
     A.tickets = P.cw_tk.as<dev::CwTicket>();
     A.nch = P.cw_nch.as<int32_t>();
@@ -2670,7 +2800,7 @@ int csrc_gpu_plan_get_info(csrc_gpu_plan_t plan, csrc_gpu_plan_info* info) {
         for (const DevBuf* d : {&P.ia, &P.ja, &P.al, &P.au, &P.ad, &P.sched, &P.cta_ptr,
                                 &P.band_shift, &P.tile_band, &P.band_rs, &P.spill_shift, &P.buf, &P.boff, &P.blo, &P.bhi, &P.bstart,
                                 &P.iv_begin, &P.iv_end, &P.cptr, &P.contrib, &P.rid, &P.cia,
-                                &P.cja, &P.cal, &P.cau, &P.cad, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t, &P.xs_tab, &P.xs_clo, &P.xs_chi, &P.xs_cbase})
+                                &P.cja, &P.cal, &P.cau, &P.cad, &P.cpk, &P.cw_xp, &P.cw_yp, &P.cw_tk, &P.eptr, &P.eidx, &P.eval, &P.eval_t, &P.pbase, &P.pat_off, &P.dx, &P.dy, &P.dxd, &P.dyd, &P.rt_ptr, &P.rt_col, &P.rt_val, &P.sbase, &P.rmeta, &P.sidx, &P.sval, &P.sval_t, &P.xs_tab, &P.xs_clo, &P.xs_chi, &P.xs_cbase})
             if (d->p) dbytes += d->bytes;
         info->device_bytes = static_cast<int64_t>(dbytes);
         info->n_windows = P.exec_kind == CSRC_KIND_WINDOWED || P.exec_kind == CSRC_KIND_LOCAL_BUFFERS

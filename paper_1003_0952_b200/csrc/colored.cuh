@@ -73,7 +73,7 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
 }
 __device__ __forceinline__ int ld_acquire(const int32_t* p) {
     int v;
-    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 
@@ -202,6 +202,368 @@ __global__ void __launch_bounds__(NT, MINB) k_colored_wave(ColorWaveArgs<T> A) {
             __threadfence();
             atomicAdd(A.ctr + 1 + task, 1);
         }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Ring form of the wavefront (the default): the same (class, block) tasks,
+// tickets and dependency counters, but every CTA is warp-specialised. One
+// producer warp takes tickets ahead of time and streams each chunk's pairs --
+// packed per sub-chunk as [ja | al | au], SELL-128 -- into a shared-memory ring
+// with one TMA bulk copy per stage (L2 evict_first: the matrix is read once);
+// four consumer warps (one row per thread) wait for the stage, then for the
+// chunk's dependencies, and only then touch xp / yp in L2. The DRAM latency of
+// the matrix stream is therefore off the dependency path: the rows "in flight"
+// for the wavefront are just the ~300 chunks in their L2 read-add-write phase,
+// so class e can trail class e-1 by little more than the bandwidth and the
+// x / y window of all classes (~ (C + 2) (bw + in-flight rows) 16 B) stays
+// L2-resident. A control warp polls the dependencies ahead of the consumers and
+// publishes the completion counts behind them (need = 4 per chunk); there is no
+// CTA-wide barrier in the loop.
+constexpr int kCrRows = 128;       // rows per chunk = consumer threads
+constexpr int kCrWarps = kCrRows / 32;
+constexpr int kCrMaxStages = 6;
+constexpr int kCrCopy = 1024;     // positions per copy chunk (tasks e = 0 and e = C + 1)
+
+struct __align__(16) CrHdr {
+    int32_t task, r0, r1, e;
+    int32_t nq, flags, pad0, pad1;  // flags: 1 first sub-chunk, 2 last
+};
+
+template <typename T>
+struct ColorRingArgs {
+    const CwTicket* tickets;   // ebase = byte offset of the chunk in pk; pad = entries per sub-chunk
+    const int32_t* nch;        // chunks per task
+    int32_t* ctr;              // [0] ticket counter, [1 + task] finished consumer warps
+    int32_t n_tickets, n_blocks, n_e, radius;
+    const int32_t* rid;
+    const unsigned char* pk;   // packed pairs
+    const T* ad;
+    const T* x;
+    T* y;
+    T* xp;
+    T* yp;
+    int32_t stages, stage_bytes;
+    int32_t sym;               // no au section (value-symmetric)
+    int32_t tr;                // transpose product: al / au roles swapped
+};
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void tma_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// xp / yp accesses: L2 only (other SMs write them within the launch); HINT adds an
+// evict_last policy so the wavefront window outlives the matrix stream in L2
+template <bool HINT>
+__device__ __forceinline__ double ld_w(const double* p, uint64_t pol) {
+    double v;
+    if (HINT)
+        asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+template <bool HINT>
+__device__ __forceinline__ float ld_w(const float* p, uint64_t pol) {
+    float v;
+    if (HINT)
+        asm volatile("ld.global.cg.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    else
+        asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+template <bool HINT>
+__device__ __forceinline__ void st_w(double* p, double v, uint64_t pol) {
+    if (HINT)
+        asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol));
+    else
+        asm volatile("st.global.cg.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+template <bool HINT>
+__device__ __forceinline__ void st_w(float* p, float v, uint64_t pol) {
+    if (HINT)
+        asm volatile("st.global.cg.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol));
+    else
+        asm volatile("st.global.cg.f32 [%0], %1;" ::"l"(p), "f"(v));
+}
+
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+constexpr int kCrThreads = kCrRows + 64;  // consumers + loader warp + control warp
+
+// Warp roles: consumers 0 .. kCrWarps-1 (one row per thread), loader kCrWarps
+// (lane 0: tickets, TMA), control kCrWarps + 1 (dependency polls ahead of the
+// consumers; fence + completion count behind them). Per stage s:
+//   pub[s]   loader -> control   the fill's header is written
+//   full[s]  loader (TMA bytes) + control (dependencies met) -> consumers
+//   done[s]  consumers -> loader (stage free) and control (stores issued)
+// so a consumer warp's chain per sub-chunk is one L2 round trip: wait full,
+// gather x / y, store, arrive done. The poll's round trip runs while the TMA is
+// in flight, the fence's while the consumers are on their next chunk.
+template <typename T, int U, bool HINT>
+__global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_colored_ring(ColorRingArgs<T> A) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t full[kCrMaxStages];
+    __shared__ __align__(8) uint64_t done[kCrMaxStages];
+    __shared__ __align__(8) uint64_t pub[kCrMaxStages];
+    __shared__ CrHdr hdr[kCrMaxStages];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int S = A.stages;
+    if (tid == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 2);
+            mbar_init(&done[s], kCrWarps);
+            mbar_init(&pub[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kCrWarps) {
+        // --------------------------------------------------------- loader
+        if (lane != 0) return;
+        const uint64_t pol = l2_policy_evict_first();
+        const int n = A.n_tickets;
+        const uint32_t eb = 4u + static_cast<uint32_t>(sizeof(T)) * (A.sym ? 1u : 2u);  // bytes per pair
+        int idx = atomicAdd(A.ctr, 1);
+        int nxt = atomicAdd(A.ctr, 1);
+        bool have = idx < n;
+        CwTicket tk{};
+        if (have) tk = A.tickets[idx];
+        int fill = 0;
+        for (;;) {
+            // the next ticket and the index after it are fetched while this one streams
+            const bool have_n = nxt < n;
+            CwTicket tkn{};
+            if (have_n) tkn = A.tickets[nxt];
+            const int nn = have_n ? atomicAdd(A.ctr, 1) : n;
+            if (!have) {
+                const int s = fill % S;
+                mbar_wait(&done[s], ((fill / S) & 1) ^ 1);
+                hdr[s].task = -1;
+                mbar_arrive(&pub[s]);
+                mbar_arrive(&full[s]);
+                break;
+            }
+            const bool cls = tk.e >= 1 && tk.e < A.n_e - 1 && tk.w > 0;
+            const int ws = cls ? tk.pad : 1;
+            const int nsub = cls ? (tk.w + ws - 1) / ws : 1;
+            const unsigned char* src = A.pk + tk.ebase;
+            for (int k = 0; k < nsub; ++k, ++fill) {
+                const int s = fill % S;
+                mbar_wait(&done[s], ((fill / S) & 1) ^ 1);
+                const int nq = cls ? min(ws, tk.w - k * ws) : 0;
+                CrHdr h;
+                h.task = tk.task;
+                h.r0 = tk.r0;
+                h.r1 = tk.r1;
+                h.e = tk.e;
+                h.nq = nq;
+                h.flags = (k == 0 ? 1 : 0) | (k == nsub - 1 ? 2 : 0);
+                h.pad0 = h.pad1 = 0;
+                hdr[s] = h;
+                mbar_arrive(&pub[s]);
+                if (nq) {
+                    const uint32_t bytes = static_cast<uint32_t>(nq) * kCrRows * eb;
+                    mbar_expect_tx(&full[s], bytes);
+                    tma_load_hint(smem_raw + static_cast<size_t>(s) * A.stage_bytes, src, bytes, &full[s], pol);
+                    src += bytes;
+                } else {
+                    mbar_arrive(&full[s]);
+                }
+            }
+            tk = tkn;
+            have = have_n;
+            nxt = nn;
+        }
+        return;
+    }
+
+    if (warp == kCrWarps + 1) {
+        // -------------------------------------------------------- control
+        // never blocks on one thing: a chunk of this CTA that is waiting for its
+        // dependencies must not hold back the completion counts of earlier chunks
+        // (on small matrices a chunk can depend on one this CTA ran itself)
+        __shared__ int32_t sig_task[kCrMaxStages];
+        int fc = 0, fs = 0;       // next fill to release / to count as finished
+        bool pending = false, stop = false, need_dep = false;
+        int dep = -1, need = 0;
+        while (!(stop && fs == fc)) {
+            bool prog = false;
+            // fill fc reuses the stage of fill fc - S: its completion must be counted first
+            // (sig_task[s] and the done[s] phase parity are per stage)
+            if (!stop && !pending && fc - fs < S) {
+                const int s = fc % S;
+                int got = 0;
+                if (lane == 0) got = mbar_try(&pub[s], (fc / S) & 1) ? 1 : 0;
+                got = __shfl_sync(0xffffffffu, got, 0);
+                if (got) {
+                    const CrHdr h = hdr[s];
+                    if (h.task < 0) {
+                        stop = true;
+                        if (lane == 0) mbar_arrive(&full[s]);  // the consumers read the stop marker
+                    } else {
+                        if (lane == 0) sig_task[s] = (h.flags & 2) ? h.task : -1;
+                        pending = true;
+                        need_dep = (h.flags & 1) && h.e >= 1;
+                        dep = -1;
+                        if (need_dep) {
+                            // (e-1, b-R .. b+R): every earlier task that may share a written y position
+                            const int b = h.task % A.n_blocks;
+                            const int d = b - A.radius + lane;
+                            if (lane <= 2 * A.radius && d >= 0 && d < A.n_blocks) {
+                                dep = (h.e - 1) * A.n_blocks + d;
+                                need = __ldg(A.nch + dep) * kCrWarps;
+                            }
+                        }
+                    }
+                    prog = true;
+                }
+            }
+            if (pending) {
+                bool ok = true;
+                if (need_dep) {
+                    const bool mine = dep < 0 || ld_acquire(A.ctr + 1 + dep) >= need;
+                    if (mine) dep = -1;  // met once, met for good (the counts only grow)
+                    ok = __all_sync(0xffffffffu, mine);
+                }
+                if (ok) {
+                    if (lane == 0) mbar_arrive(&full[fc % S]);
+                    pending = false;
+                    ++fc;
+                    prog = true;
+                }
+            }
+            if (fs < fc) {
+                const int s = fs % S;
+                int got = 0;
+                if (lane == 0) got = mbar_try(&done[s], (fs / S) & 1) ? 1 : 0;
+                got = __shfl_sync(0xffffffffu, got, 0);
+                if (got) {
+                    if (lane == 0) {
+                        const int t = sig_task[s];
+                        if (t >= 0) {
+                            __threadfence();  // the consumers' stores (ordered before lane 0 by done[s]) precede the count
+                            atomicAdd(A.ctr + 1 + t, kCrWarps);
+                        }
+                    }
+                    __syncwarp();
+                    ++fs;
+                    prog = true;
+                }
+            }
+            if (!prog) __nanosleep(20);
+        }
+        return;
+    }
+
+    // ----------------------------------------------------------- consumers
+    const uint64_t pol = HINT ? l2_policy_evict_last() : 0;
+    T xi = T(0), acc = T(0), yown = T(0);
+    for (int fill = 0;; ++fill) {
+        const int s = fill % S;
+        mbar_wait(&full[s], (fill / S) & 1);
+        const CrHdr h = hdr[s];
+        if (h.task < 0) return;
+        const int e = h.e;
+        const int r = h.r0 + tid;
+        const bool cls = e >= 1 && e < A.n_e - 1;
+        if (e == 0) {
+            // x -> class-major xp, zero yp (block b, all classes); a copy chunk holds
+            // <= kCrCopy positions, so every thread's loads go out together
+            int32_t i[kCrCopy / kCrRows];
+            T v[kCrCopy / kCrRows];
+#pragma unroll
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) {
+                const int q = r + u * kCrRows;
+                i[u] = q < h.r1 ? __ldg(A.rid + q) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) v[u] = i[u] >= 0 ? __ldg(A.x + i[u]) : T(0);
+#pragma unroll
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) {
+                const int q = r + u * kCrRows;
+                if (q < h.r1) {
+                    st_w<HINT>(A.xp + q, v[u], pol);
+                    st_w<HINT>(A.yp + q, T(0), pol);
+                }
+            }
+        } else if (!cls) {
+            // class-major yp -> y (block b): final once every class of blocks b .. b+R is done
+            int32_t i[kCrCopy / kCrRows];
+            T v[kCrCopy / kCrRows];
+#pragma unroll
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) {
+                const int q = r + u * kCrRows;
+                i[u] = q < h.r1 ? __ldg(A.rid + q) : -1;
+                v[u] = q < h.r1 ? ld_w<HINT>(A.yp + q, pol) : T(0);
+            }
+#pragma unroll
+            for (int u = 0; u < kCrCopy / kCrRows; ++u)
+                if (i[u] >= 0) A.y[i[u]] = v[u];
+        } else {
+            // one row per thread: colorful_worker's row update (parallel.hpp:411-434)
+            const bool act = r < h.r1;
+            if (h.flags & 1) {
+                xi = act ? ld_w<HINT>(A.xp + r, pol) : T(0);
+                yown = act ? ld_w<HINT>(A.yp + r, pol) : T(0);  // no other row of this class writes y[r]
+                acc = T(0);
+            }
+            const int nq = h.nq;
+            const unsigned char* st = smem_raw + static_cast<size_t>(s) * A.stage_bytes;
+            const int32_t* sja = reinterpret_cast<const int32_t*>(st) + tid;
+            const T* sv0 = reinterpret_cast<const T*>(st + static_cast<size_t>(nq) * kCrRows * 4) + tid;
+            const T* sv1 = A.sym ? sv0 : sv0 + static_cast<size_t>(nq) * kCrRows;
+            const T* sal = A.tr ? sv1 : sv0;
+            const T* sau = A.tr ? sv0 : sv1;
+            for (int q0 = 0; q0 < nq; q0 += U) {
+                int32_t j[U];
+                T xv[U], yv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) j[u] = q0 + u < nq ? sja[(q0 + u) * kCrRows] : r;
+                // padding entries (own row) neither gather nor scatter
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool real = j[u] != r;
+                    xv[u] = real ? ld_w<HINT>(A.xp + j[u], pol) : T(0);
+                    yv[u] = real ? ld_w<HINT>(A.yp + j[u], pol) : T(0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (j[u] != r) {
+                        acc = fma(sal[(q0 + u) * kCrRows], xv[u], acc);
+                        st_w<HINT>(A.yp + j[u], fma(sau[(q0 + u) * kCrRows], xi, yv[u]), pol);
+                    }
+                }
+            }
+            if ((h.flags & 2) && act) st_w<HINT>(A.yp + r, yown + fma(__ldg(A.ad + r), xi, acc), pol);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&done[s]);  // stage free (loader), stores issued (control)
     }
 }
 

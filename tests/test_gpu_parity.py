@@ -852,3 +852,46 @@ def test_permuted_mesh_has_no_small_dictionary():
     ex = P.GpuSpmv(a, P.Strategy(K.gather))
     assert ex.info().row_patterns == 0
     ex.close()
+
+
+COLORED_SHAPES = [
+    {},                                                                   # ring form, defaults
+    {"CSRC_GPU_CW_RING": "0"},                                            # direct wavefront (no TMA ring)
+    {"CSRC_GPU_COLOR_WAVE": "0"},                                         # one launch per class
+    {"CSRC_GPU_CR_STAGE_BYTES": "2560", "CSRC_GPU_CW_U": "4"},            # 1-pair sub-chunks: many fills per chunk
+    {"CSRC_GPU_CR_STAGE_BYTES": "7680", "CSRC_GPU_CR_STAGES": "3", "CSRC_GPU_CW_U": "8"},
+    {"CSRC_GPU_CR_STAGES": "6", "CSRC_GPU_CW_U": "16"},
+    {"CSRC_GPU_CR_HINT": "1"},                                            # evict_last on the x / y window
+    {"CSRC_GPU_CW_R": "1", "CSRC_GPU_CW_D": "2"},                         # tightest dependency distance
+    {"CSRC_GPU_CW_R": "8", "CSRC_GPU_CW_MINB": "1"},                      # many small blocks, radius 8
+    {"CSRC_GPU_CW_CTAS": "1"},                                            # one CTA per SM
+]
+
+
+@pytest.mark.parametrize("env", COLORED_SHAPES, ids=lambda e: ",".join(f"{k[9:]}={v}" for k, v in e.items()) or "default")
+def test_colored_kernel_shapes(env, monkeypatch):
+    """Every form / shape of the colored kernel (colored.cuh): the TMA-ring
+    wavefront (default), the direct wavefront and the launch-per-class form,
+    with stage sizes that split chunks into many sub-chunks, every U, deep and
+    shallow rings, tight and wide dependency windows -- y and y^T against the
+    oracle on the golden meshes (fp64 and fp32), bit-identical repeats (no
+    atomics), and the reference's class-order result on the family."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    for key in ("g1_", "g2_", "g3_", "g4_"):
+        a = MESH.matrix(key)
+        x = MESH[key + "x"]
+        for mode in (P.ConflictMode.neighborhood, P.ConflictMode.exact):
+            ex = P.GpuSpmv(a, P.Strategy(K.colorful, p=4, conflict_mode=mode))
+            y = ex.apply(x)
+            assert rel_l2(y, MESH[key + "y"]) <= TOL64, (key, mode)
+            assert np.array_equal(ex.apply(x), y), (key, mode)
+            assert rel_l2(ex.apply(x, transpose=True), O.spmv_csrc(a, x, transpose=True)) <= TOL64, (key, mode)
+            ex.close()
+        x32 = x.astype(np.float32).astype(np.float64)
+        y32 = run(a, x32, P.Strategy(K.colorful, p=4, dtype=P.DType.f32))
+        assert rel_l2(y32, O.spmv_csrc(round32(a), x32)) <= TOL32, key
+    for idx in (0, 7, 19, 25, 28):
+        p = f"m{idx}_"
+        a = FAM.matrix(p)
+        assert rel_l2(run(a, FAM[p + "x"], P.Strategy(K.colorful, p=3)), FAM[p + "y"]) <= TOL64, idx
