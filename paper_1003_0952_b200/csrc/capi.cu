@@ -234,7 +234,7 @@ struct csrc_gpu_plan_s {
     DevBuf cw_tk, cw_nch, cw_ctr, cw_xp, cw_yp;
     // ring form (k_colored_ring): pairs packed per sub-chunk, TMA-staged
     bool cw_ring = false;
-    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0;
+    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0, cr_split = 0;
     DevBuf cpk;
 
     // host-path scratch
@@ -770,23 +770,22 @@ const void* colored_wave_fn(const Plan& P) {
     return P.cw_nt == 256 ? colored_wave_fn_nt<T, 256>(P.cw_u) : colored_wave_fn_nt<T, 128>(P.cw_u);
 }
 
-template <class T>
-const void* colored_ring_fn(const Plan& P) {
-    if (P.cr_hint) {
-        switch (P.cw_u) {
-            case 16: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 16, true>);
-            case 14: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 14, true>);
-            case 4: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 4, true>);
-            default: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, true>);
-        }
-    }
-    switch (P.cw_u) {
-        case 16: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 16, false>);
-        case 14: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 14, false>);
-        case 4: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 4, false>);
-        default: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, false>);
+template <class T, bool HINT, bool SPLIT>
+const void* colored_ring_fn_hs(int u) {
+    switch (u) {
+        case 16: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 16, HINT, SPLIT>);
+        case 14: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 14, HINT, SPLIT>);
+        case 4: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 4, HINT, SPLIT>);
+        default: return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, HINT, SPLIT>);
     }
 }
+template <class T>
+const void* colored_ring_fn(const Plan& P) {
+    if (P.cr_split)
+        return P.cr_hint ? colored_ring_fn_hs<T, true, true>(P.cw_u) : colored_ring_fn_hs<T, false, true>(P.cw_u);
+    return P.cr_hint ? colored_ring_fn_hs<T, true, false>(P.cw_u) : colored_ring_fn_hs<T, false, false>(P.cw_u);
+}
+int colored_ring_threads(const Plan& P) { return P.cr_split ? dev::kCrSplitThreads : dev::kCrThreads; }
 
 template <class T>
 void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& color, int C) {
@@ -796,20 +795,22 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
         if (a.ia[i + 1] > a.ia[i]) bw = std::max<count_t>(bw, i - a.ja[a.ia[i]]);
     {
         P.cw_ring = env_int("CSRC_GPU_CW_RING", 1) != 0;
-        const int u = env_int("CSRC_GPU_CW_U", P.cw_ring ? 14 : 8);
+        const int u = env_int("CSRC_GPU_CW_U", 8);
         P.cw_u = (u == 4 || u == 16 || (u == 14 && P.cw_ring)) ? u : 8;
         P.cw_nt = env_int("CSRC_GPU_CW_NT", 128) == 256 ? 256 : 128;
         P.cw_pf = env_int("CSRC_GPU_CW_PF", 1);
         if (P.cw_ring) P.cw_nt = dev::kCrRows;
         P.cr_stages = std::min(dev::kCrMaxStages, std::max(2, env_int("CSRC_GPU_CR_STAGES", 2)));
         P.cr_hint = env_int("CSRC_GPU_CR_HINT", 0) != 0;
+        P.cr_split = env_int("CSRC_GPU_CR_SPLIT", 0) != 0;
     }
     const bool ring = P.cw_ring;
     // ring form: bytes per stored pair, pairs per row a stage holds (one sub-chunk)
     const int64_t pair_bytes = 4 + static_cast<int64_t>(sizeof(T)) * (a.value_symmetric ? 1 : 2);
     const int ws_max = static_cast<int>(std::max<int64_t>(
         1, static_cast<int64_t>(env_int("CSRC_GPU_CR_STAGE_BYTES", 33280)) / (dev::kCrRows * pair_bytes)));
-    P.cr_stage_bytes = static_cast<int>(ws_max * dev::kCrRows * pair_bytes);
+    // (a copy chunk stages its kCrCopy row ids in the same ring)
+    P.cr_stage_bytes = std::max<int>(static_cast<int>(ws_max * dev::kCrRows * pair_bytes), dev::kCrCopy * 4);
     // blocks of B rows, R = ceil(bw / B): rows more than R blocks apart never write the
     // same y position (row i writes only on [i - bw, i])
     const int r_target = std::min(15, std::max(1, env_int("CSRC_GPU_CW_R", 4)));
@@ -988,7 +989,7 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     const int smem = ring ? P.cr_stages * P.cr_stage_bytes : 0;
     if (ring) set_smem_limit(fn, smem);
     int occ = 0;
-    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ring ? dev::kCrThreads : P.cw_nt, smem));
+    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, ring ? colored_ring_threads(P) : P.cw_nt, smem));
     const int per_sm = env_int("CSRC_GPU_CW_CTAS", std::max(occ, 1));
     const int grid_max = num_sms(P.device) * std::min(per_sm, std::max(occ, 1));
     int d_default = 4 * R;
@@ -2183,7 +2184,7 @@ void launch_colored_ring(const Plan& P, bool tr, const T* x, T* y, cudaStream_t 
     const int smem = P.cr_stages * P.cr_stage_bytes;
     set_smem_limit(fn, smem);
     void* args[] = {&A};
-    CUDA_OK(cudaLaunchKernel(fn, dim3(P.cw_grid), dim3(dev::kCrThreads), args, smem, st));
+    CUDA_OK(cudaLaunchKernel(fn, dim3(P.cw_grid), dim3(colored_ring_threads(P)), args, smem, st));
 }
 
 template <class T>

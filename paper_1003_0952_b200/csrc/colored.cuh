@@ -237,7 +237,7 @@ struct ColorRingArgs {
     const int32_t* nch;        // chunks per task
     int32_t* ctr;              // [0] ticket counter, [1 + task] finished consumer warps
     int32_t n_tickets, n_blocks, n_e, radius;
-    const int32_t* rid;
+    const int32_t* rid;        // class-major row -> natural row (-1: padding)
     const unsigned char* pk;   // packed pairs
     const T* ad;
     const T* x;
@@ -311,19 +311,30 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
-constexpr int kCrThreads = kCrRows + 64;  // consumers + loader warp + control warp
+constexpr int kCrThreads = kCrRows + 96;  // consumers + loader, checker and signaller warps
+// SPLIT form: 256 threads (a second warpgroup of the three helper warps + one idle warp)
+// and a setmaxnreg register split -- the launch gives every thread 80 registers (3 CTAs per
+// SM), the helper warpgroup drops to 40 and the consumers rise to 120, so the U = 14 / 16
+// forms (a whole 27-point row's gathers in flight: one L2 round trip per chunk) keep three
+// CTAs per SM instead of two.
+constexpr int kCrSplitThreads = 2 * kCrRows;
+constexpr int kCrHelperRegs = 40;
+constexpr int kCrConsumerRegs = 120;
 
 // Warp roles: consumers 0 .. kCrWarps-1 (one row per thread), loader kCrWarps
-// (lane 0: tickets, TMA), control kCrWarps + 1 (dependency polls ahead of the
-// consumers; fence + completion count behind them). Per stage s:
-//   pub[s]   loader -> control   the fill's header is written
-//   full[s]  loader (TMA bytes) + control (dependencies met) -> consumers
-//   done[s]  consumers -> loader (stage free) and control (stores issued)
+// (lane 0: tickets, TMA), checker kCrWarps + 1 (dependency polls ahead of the
+// consumers), signaller kCrWarps + 2 (fence + completion count behind them).
+// Per stage s:
+//   pub[s]   loader -> checker, signaller   the fill's header is written
+//   full[s]  loader (TMA bytes) + checker (dependencies met) -> consumers
+//   done[s]  consumers + signaller (header read) -> loader (stage free) and
+//            signaller (stores issued)
 // so a consumer warp's chain per sub-chunk is one L2 round trip: wait full,
 // gather x / y, store, arrive done. The poll's round trip runs while the TMA is
 // in flight, the fence's while the consumers are on their next chunk.
-template <typename T, int U, bool HINT>
-__global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_colored_ring(ColorRingArgs<T> A) {
+template <typename T, int U, bool HINT, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 3 : (U <= 4 ? 4 : (U <= 8 ? 3 : 2)))
+    k_colored_ring(ColorRingArgs<T> A) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kCrMaxStages];
     __shared__ __align__(8) uint64_t done[kCrMaxStages];
@@ -336,13 +347,14 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);
-            mbar_init(&done[s], kCrWarps);
+            mbar_init(&done[s], kCrWarps + 1);
             mbar_init(&pub[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
+    if (SPLIT && warp >= kCrWarps) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kCrHelperRegs));
     if (warp == kCrWarps) {
         // --------------------------------------------------------- loader
         if (lane != 0) return;
@@ -392,6 +404,11 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
                     mbar_expect_tx(&full[s], bytes);
                     tma_load_hint(smem_raw + static_cast<size_t>(s) * A.stage_bytes, src, bytes, &full[s], pol);
                     src += bytes;
+                } else if (!cls && tk.r1 > tk.r0 && (tk.e == 0 || tk.e == A.n_e - 1)) {
+                    // copy chunk: its row ids (32-aligned start, 16-byte granular length; rid is padded)
+                    const uint32_t bytes = (static_cast<uint32_t>(tk.r1 - tk.r0) * 4u + 15u) & ~15u;
+                    mbar_expect_tx(&full[s], bytes);
+                    tma_load_hint(smem_raw + static_cast<size_t>(s) * A.stage_bytes, A.rid + tk.r0, bytes, &full[s], pol);
                 } else {
                     mbar_arrive(&full[s]);
                 }
@@ -404,86 +421,58 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
     }
 
     if (warp == kCrWarps + 1) {
-        // -------------------------------------------------------- control
-        // never blocks on one thing: a chunk of this CTA that is waiting for its
-        // dependencies must not hold back the completion counts of earlier chunks
-        // (on small matrices a chunk can depend on one this CTA ran itself)
-        __shared__ int32_t sig_task[kCrMaxStages];
-        int fc = 0, fs = 0;       // next fill to release / to count as finished
-        bool pending = false, stop = false, need_dep = false;
-        int dep = -1, need = 0;
-        while (!(stop && fs == fc)) {
-            bool prog = false;
-            // fill fc reuses the stage of fill fc - S: its completion must be counted first
-            // (sig_task[s] and the done[s] phase parity are per stage)
-            if (!stop && !pending && fc - fs < S) {
-                const int s = fc % S;
-                int got = 0;
-                if (lane == 0) got = mbar_try(&pub[s], (fc / S) & 1) ? 1 : 0;
-                got = __shfl_sync(0xffffffffu, got, 0);
-                if (got) {
-                    const CrHdr h = hdr[s];
-                    if (h.task < 0) {
-                        stop = true;
-                        if (lane == 0) mbar_arrive(&full[s]);  // the consumers read the stop marker
-                    } else {
-                        if (lane == 0) sig_task[s] = (h.flags & 2) ? h.task : -1;
-                        pending = true;
-                        need_dep = (h.flags & 1) && h.e >= 1;
-                        dep = -1;
-                        if (need_dep) {
-                            // (e-1, b-R .. b+R): every earlier task that may share a written y position
-                            const int b = h.task % A.n_blocks;
-                            const int d = b - A.radius + lane;
-                            if (lane <= 2 * A.radius && d >= 0 && d < A.n_blocks) {
-                                dep = (h.e - 1) * A.n_blocks + d;
-                                need = __ldg(A.nch + dep) * kCrWarps;
-                            }
-                        }
-                    }
-                    prog = true;
+        // -------------------------------------------------------- checker
+        // polls a chunk's dependencies while its pairs are in flight, then gives full[s]
+        // its second arrival. Blocking here only delays this CTA's later fills, which
+        // its consumers take in order anyway.
+        for (int fc = 0;; ++fc) {
+            const int s = fc % S;
+            if (lane == 0) mbar_wait(&pub[s], (fc / S) & 1);
+            __syncwarp();
+            const CrHdr h = hdr[s];
+            if (h.task >= 0 && (h.flags & 1) && h.e >= 1) {
+                // (e-1, b-R .. b+R): every earlier task that may share a written y position
+                const int b = h.task % A.n_blocks;
+                const int d = b - A.radius + lane;
+                if (lane <= 2 * A.radius && d >= 0 && d < A.n_blocks) {
+                    const int dep = (h.e - 1) * A.n_blocks + d;
+                    const int need = __ldg(A.nch + dep) * kCrWarps;
+                    while (ld_acquire(A.ctr + 1 + dep) < need) __nanosleep(20);
                 }
             }
-            if (pending) {
-                bool ok = true;
-                if (need_dep) {
-                    const bool mine = dep < 0 || ld_acquire(A.ctr + 1 + dep) >= need;
-                    if (mine) dep = -1;  // met once, met for good (the counts only grow)
-                    ok = __all_sync(0xffffffffu, mine);
-                }
-                if (ok) {
-                    if (lane == 0) mbar_arrive(&full[fc % S]);
-                    pending = false;
-                    ++fc;
-                    prog = true;
-                }
-            }
-            if (fs < fc) {
-                const int s = fs % S;
-                int got = 0;
-                if (lane == 0) got = mbar_try(&done[s], (fs / S) & 1) ? 1 : 0;
-                got = __shfl_sync(0xffffffffu, got, 0);
-                if (got) {
-                    if (lane == 0) {
-                        const int t = sig_task[s];
-                        if (t >= 0) {
-                            __threadfence();  // the consumers' stores (ordered before lane 0 by done[s]) precede the count
-                            atomicAdd(A.ctr + 1 + t, kCrWarps);
-                        }
-                    }
-                    __syncwarp();
-                    ++fs;
-                    prog = true;
-                }
-            }
-            if (!prog) __nanosleep(20);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[s]);  // (stop marker: the consumers read it and leave)
+            if (h.task < 0) return;
         }
-        return;
     }
 
+    if (warp == kCrWarps + 2) {
+        // ------------------------------------------------------ signaller
+        // publishes completion counts behind the consumers, so the fence's round trip is
+        // on nobody's critical path. It holds one of done[s]'s arrivals until it has read
+        // the fill's header, which keeps the loader from overwriting hdr[s] before that.
+        if (lane != 0) return;
+        for (int fs = 0;; ++fs) {
+            const int s = fs % S;
+            mbar_wait(&pub[s], (fs / S) & 1);
+            const int task = hdr[s].task;
+            const int flags = hdr[s].flags;
+            if (task < 0) return;
+            mbar_arrive(&done[s]);
+            mbar_wait(&done[s], (fs / S) & 1);
+            if (flags & 2) {
+                __threadfence();  // the consumers' stores (ordered before this thread by done[s]) precede the count
+                atomicAdd(A.ctr + 1 + task, kCrWarps);
+            }
+        }
+    }
+
+    if (warp > kCrWarps + 2) return;  // SPLIT: the helper warpgroup's spare warp
+
     // ----------------------------------------------------------- consumers
+    if (SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kCrConsumerRegs));
     const uint64_t pol = HINT ? l2_policy_evict_last() : 0;
-    T xi = T(0), acc = T(0), yown = T(0);
+    T xi = T(0), acc = T(0), yown = T(0), dr = T(0);
     for (int fill = 0;; ++fill) {
         const int s = fill % S;
         mbar_wait(&full[s], (fill / S) & 1);
@@ -493,17 +482,16 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
         const int r = h.r0 + tid;
         const bool cls = e >= 1 && e < A.n_e - 1;
         if (e == 0) {
-            // x -> class-major xp, zero yp (block b, all classes); a copy chunk holds
-            // <= kCrCopy positions, so every thread's loads go out together
+            // x -> class-major xp, zero yp (block b, all classes). The loader staged the
+            // chunk's row ids with the ring, so the only global round trip is x itself; a
+            // copy chunk holds <= kCrCopy positions and every thread's loads go out together
+            const int32_t* srid = reinterpret_cast<const int32_t*>(smem_raw + static_cast<size_t>(s) * A.stage_bytes) + tid;
             int32_t i[kCrCopy / kCrRows];
             T v[kCrCopy / kCrRows];
 #pragma unroll
-            for (int u = 0; u < kCrCopy / kCrRows; ++u) {
-                const int q = r + u * kCrRows;
-                i[u] = q < h.r1 ? __ldg(A.rid + q) : -1;
-            }
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) i[u] = r + u * kCrRows < h.r1 ? srid[u * kCrRows] : -1;
 #pragma unroll
-            for (int u = 0; u < kCrCopy / kCrRows; ++u) v[u] = i[u] >= 0 ? __ldg(A.x + i[u]) : T(0);
+            for (int u = 0; u < kCrCopy / kCrRows; ++u) v[u] = i[u] >= 0 ? __ldcs(A.x + i[u]) : T(0);  // read once: streaming
 #pragma unroll
             for (int u = 0; u < kCrCopy / kCrRows; ++u) {
                 const int q = r + u * kCrRows;
@@ -514,23 +502,25 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
             }
         } else if (!cls) {
             // class-major yp -> y (block b): final once every class of blocks b .. b+R is done
+            const int32_t* srid = reinterpret_cast<const int32_t*>(smem_raw + static_cast<size_t>(s) * A.stage_bytes) + tid;
             int32_t i[kCrCopy / kCrRows];
             T v[kCrCopy / kCrRows];
 #pragma unroll
             for (int u = 0; u < kCrCopy / kCrRows; ++u) {
                 const int q = r + u * kCrRows;
-                i[u] = q < h.r1 ? __ldg(A.rid + q) : -1;
+                i[u] = q < h.r1 ? srid[u * kCrRows] : -1;
                 v[u] = q < h.r1 ? ld_w<HINT>(A.yp + q, pol) : T(0);
             }
 #pragma unroll
             for (int u = 0; u < kCrCopy / kCrRows; ++u)
-                if (i[u] >= 0) A.y[i[u]] = v[u];
+                if (i[u] >= 0) __stcs(A.y + i[u], v[u]);  // written once: streaming
         } else {
             // one row per thread: colorful_worker's row update (parallel.hpp:411-434)
             const bool act = r < h.r1;
             if (h.flags & 1) {
                 xi = act ? ld_w<HINT>(A.xp + r, pol) : T(0);
                 yown = act ? ld_w<HINT>(A.yp + r, pol) : T(0);  // no other row of this class writes y[r]
+                dr = act ? __ldcs(A.ad + r) : T(0);
                 acc = T(0);
             }
             const int nq = h.nq;
@@ -560,10 +550,10 @@ __global__ void __launch_bounds__(kCrThreads, U <= 8 ? 4 : (U <= 14 ? 3 : 2)) k_
                     }
                 }
             }
-            if ((h.flags & 2) && act) st_w<HINT>(A.yp + r, yown + fma(__ldg(A.ad + r), xi, acc), pol);
+            if ((h.flags & 2) && act) st_w<HINT>(A.yp + r, yown + fma(dr, xi, acc), pol);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&done[s]);  // stage free (loader), stores issued (control)
+        if (lane == 0) mbar_arrive(&done[s]);  // stage free (loader), stores issued (signaller)
     }
 }
 

@@ -865,6 +865,7 @@ COLORED_SHAPES = [
     {"CSRC_GPU_CW_R": "1", "CSRC_GPU_CW_D": "2"},                         # tightest dependency distance
     {"CSRC_GPU_CW_R": "8", "CSRC_GPU_CW_MINB": "1"},                      # many small blocks, radius 8
     {"CSRC_GPU_CW_CTAS": "1"},                                            # one CTA per SM
+    {"CSRC_GPU_CR_SPLIT": "1", "CSRC_GPU_CW_U": "14"},                    # setmaxnreg register split
 ]
 
 
