@@ -290,7 +290,7 @@ KERNEL_NAMES = {1: "k_gather_rows", 2: "k_gather_staged", 3: "k_gather_sell"}
 def kernel_name(info, kind):
     if kind == "gather":
         return KERNEL_NAMES.get(int(info.gather_form), "k_gather")
-    return {"windowed": "k_windowed", "atomic": "k_atomic", "colorful": "k_colored_wave",
+    return {"windowed": "k_windowed", "atomic": "k_atomic", "colorful": "k_colored_ring",
             "local_buffers": "k_windowed (+ spill init / accumulate)"}[kind]
 
 

@@ -247,6 +247,7 @@ struct ColorRingArgs {
     int32_t stages, stage_bytes;
     int32_t sym;               // no au section (value-symmetric)
     int32_t tr;                // transpose product: al / au roles swapped
+    int32_t pf;                // prefetcher warp on: x / y gather targets of the next chunk warmed in L2
 };
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
@@ -311,7 +312,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
     return ok != 0;
 }
 
-constexpr int kCrThreads = kCrRows + 96;  // consumers + loader, checker and signaller warps
+constexpr int kCrThreads = kCrRows + 128;  // consumers + loader, checker, signaller and prefetcher warps
 // SPLIT form: 256 threads (a second warpgroup of the three helper warps + one idle warp)
 // and a setmaxnreg register split -- the launch gives every thread 80 registers (3 CTAs per
 // SM), the helper warpgroup drops to 40 and the consumers rise to 120, so the U = 14 / 16
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
     if (tid == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 2);
-            mbar_init(&done[s], kCrWarps + 1);
+            mbar_init(&done[s], kCrWarps + 1 + (A.pf ? 1 : 0));
             mbar_init(&pub[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -467,7 +468,35 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
         }
     }
 
-    if (warp > kCrWarps + 2) return;  // SPLIT: the helper warpgroup's spare warp
+    if (warp == kCrWarps + 3) {
+        // ----------------------------------------------------- prefetcher
+        // With a ring of >= 3 stages a chunk is usually released (pairs landed, dependencies
+        // met) while the consumers are still on the previous one. This warp walks the
+        // chunk's column ids from shared memory and touches the xp / yp lines its rows will
+        // gather (prefetch.global.L2: no data returned, no registers held), so the ~13 % of
+        // window sectors that fell out of L2 are back before the consumers' single round
+        // trip needs them. It holds one of done[s]'s arrivals while it reads the stage.
+        if (!A.pf) return;
+        for (int fp = 0;; ++fp) {
+            const int s = fp % S;
+            mbar_wait(&full[s], (fp / S) & 1);
+            const CrHdr h = hdr[s];
+            if (h.task < 0) return;
+            if (h.e >= 1 && h.e < A.n_e - 1 && h.nq > 0) {
+                const int32_t* sja = reinterpret_cast<const int32_t*>(smem_raw + static_cast<size_t>(s) * A.stage_bytes);
+                const int total = h.nq * kCrRows;
+                for (int k = lane; k < total; k += 32) {
+                    const int j = sja[k];
+                    if (j != h.r0 + (k & (kCrRows - 1))) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.xp + j));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(A.yp + j));
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&done[s]);
+        }
+    }
 
     // ----------------------------------------------------------- consumers
     if (SPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kCrConsumerRegs));

@@ -866,6 +866,8 @@ COLORED_SHAPES = [
     {"CSRC_GPU_CW_R": "8", "CSRC_GPU_CW_MINB": "1"},                      # many small blocks, radius 8
     {"CSRC_GPU_CW_CTAS": "1"},                                            # one CTA per SM
     {"CSRC_GPU_CR_SPLIT": "1", "CSRC_GPU_CW_U": "14"},                    # setmaxnreg register split
+    {"CSRC_GPU_CR_PF": "1", "CSRC_GPU_CR_STAGES": "3"},                   # L2 prefetcher warp
+    {"CSRC_GPU_CR_PF": "1", "CSRC_GPU_CR_STAGE_BYTES": "5120", "CSRC_GPU_CW_U": "4"},
 ]
 
 
