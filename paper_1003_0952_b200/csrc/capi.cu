@@ -794,6 +794,9 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     for (index_t i = 0; i < n; ++i)
         if (a.ia[i + 1] > a.ia[i]) bw = std::max<count_t>(bw, i - a.ja[a.ia[i]]);
     {
+        // The TMA-ring form is the default: C5 1.26 vs 1.72 ms for the direct form, C4 1.29 vs
+        // 1.80, C2 113 vs 240 us; on C3 (permuted + RCM: ragged rows, 54 classes) the direct
+        // form's 768 rows per SM still lead, 0.70 vs 0.78 ms (profiles/r02b_colored_c3_c4.txt)
         P.cw_ring = env_int("CSRC_GPU_CW_RING", 1) != 0;
         // ring: a whole 27-point row's gathers in one batch (C5 1.26 ms vs 1.32 at U = 8)
         const int u = env_int("CSRC_GPU_CW_U", P.cw_ring ? 14 : 8);
