@@ -234,7 +234,7 @@ struct csrc_gpu_plan_s {
     DevBuf cw_tk, cw_nch, cw_ctr, cw_xp, cw_yp;
     // ring form (k_colored_ring): pairs packed per sub-chunk, TMA-staged
     bool cw_ring = false;
-    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0, cr_split = 0, cr_pf = 0;
+    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0, cr_split = 0, cr_pf = 0, cr_claim = 0;
     DevBuf cpk;
 
     // host-path scratch
@@ -808,6 +808,7 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
         P.cr_hint = env_int("CSRC_GPU_CR_HINT", 0) != 0;
         P.cr_split = env_int("CSRC_GPU_CR_SPLIT", 0) != 0;
         P.cr_pf = env_int("CSRC_GPU_CR_PF", 0) != 0;
+        P.cr_claim = std::min(2, std::max(0, env_int("CSRC_GPU_CR_CLAIM", 0)));
     }
     const bool ring = P.cw_ring;
     // ring form: bytes per stored pair, pairs per row a stage holds (one sub-chunk)
@@ -999,7 +1000,7 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     const int grid_max = num_sms(P.device) * std::min(per_sm, std::max(occ, 1));
     int d_default = 4 * R;
     if (ring) {
-        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", 200) / 100.0;
+        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", 400) / 100.0;
         d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * dev::kCrRows) / static_cast<double>(B)));
     }
     const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", d_default));
@@ -2185,6 +2186,7 @@ void launch_colored_ring(const Plan& P, bool tr, const T* x, T* y, cudaStream_t 
     A.sym = P.value_symmetric ? 1 : 0;
     A.tr = tr ? 1 : 0;
     A.pf = P.cr_pf;
+    A.claim = P.cr_claim;
     CUDA_OK(cudaMemsetAsync(P.cw_ctr.p, 0, static_cast<size_t>(P.cw_tasks + 1) * 4, st));
     const void* fn = colored_ring_fn<T>(P);
     const int smem = P.cr_stages * P.cr_stage_bytes;

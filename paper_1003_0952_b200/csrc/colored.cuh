@@ -248,6 +248,7 @@ struct ColorRingArgs {
     int32_t sym;               // no au section (value-symmetric)
     int32_t tr;                // transpose product: al / au roles swapped
     int32_t pf;                // prefetcher warp on: x / y gather targets of the next chunk warmed in L2
+    int32_t claim;             // loader's ticket claim policy (0 eager, 1 after staging, 2 when a stage is free)
 };
 
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
@@ -362,18 +363,28 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
         const uint64_t pol = l2_policy_evict_first();
         const int n = A.n_tickets;
         const uint32_t eb = 4u + static_cast<uint32_t>(sizeof(T)) * (A.sym ? 1u : 2u);  // bytes per pair
+        // Ticket claims (A.claim): every claimed, unfinished ticket widens the distance the
+        // classes must keep (its rows count as in flight), so claiming late keeps the x / y
+        // window small; claiming early hides the counter + ticket round trips.
+        //   0  two tickets ahead of the one being staged (both round trips hidden)
+        //   1  the next ticket once the current one is staged
+        //   2  the next ticket only when a stage is free for it
         int idx = atomicAdd(A.ctr, 1);
-        int nxt = atomicAdd(A.ctr, 1);
+        int nxt = A.claim == 0 ? atomicAdd(A.ctr, 1) : n;
         bool have = idx < n;
         CwTicket tk{};
         if (have) tk = A.tickets[idx];
         int fill = 0;
         for (;;) {
-            // the next ticket and the index after it are fetched while this one streams
-            const bool have_n = nxt < n;
+            bool have_n = false;
             CwTicket tkn{};
-            if (have_n) tkn = A.tickets[nxt];
-            const int nn = have_n ? atomicAdd(A.ctr, 1) : n;
+            int nn = n;
+            if (A.claim == 0) {
+                // the next ticket and the index after it are fetched while this one streams
+                have_n = nxt < n;
+                if (have_n) tkn = A.tickets[nxt];
+                nn = have_n ? atomicAdd(A.ctr, 1) : n;
+            }
             if (!have) {
                 const int s = fill % S;
                 mbar_wait(&done[s], ((fill / S) & 1) ^ 1);
@@ -414,9 +425,16 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
                     mbar_arrive(&full[s]);
                 }
             }
-            tk = tkn;
-            have = have_n;
-            nxt = nn;
+            if (A.claim == 0) {
+                tk = tkn;
+                have = have_n;
+                nxt = nn;
+            } else {
+                if (A.claim == 2) mbar_wait(&done[fill % S], ((fill / S) & 1) ^ 1);  // a stage is free
+                idx = atomicAdd(A.ctr, 1);
+                have = idx < n;
+                if (have) tk = A.tickets[idx];
+            }
         }
         return;
     }
