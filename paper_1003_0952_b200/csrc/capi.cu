@@ -234,7 +234,7 @@ struct csrc_gpu_plan_s {
     DevBuf cw_tk, cw_nch, cw_ctr, cw_xp, cw_yp;
     // ring form (k_colored_ring): pairs packed per sub-chunk, TMA-staged
     bool cw_ring = false;
-    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0, cr_split = 0, cr_pf = 0, cr_claim = 0;
+    int cr_stages = 3, cr_stage_bytes = 0, cr_hint = 0, cr_split = 0, cr_pf = 0, cr_claim = 0, cr_lr = 1;
     DevBuf cpk;
 
     // host-path scratch
@@ -781,6 +781,7 @@ const void* colored_ring_fn_hs(int u) {
 }
 template <class T>
 const void* colored_ring_fn(const Plan& P) {
+    if (P.cr_lr == 2) return reinterpret_cast<const void*>(&dev::k_colored_ring<T, 8, false, false, 2>);
     if (P.cr_split)
         return P.cr_hint ? colored_ring_fn_hs<T, true, true>(P.cw_u) : colored_ring_fn_hs<T, false, true>(P.cw_u);
     return P.cr_hint ? colored_ring_fn_hs<T, true, false>(P.cw_u) : colored_ring_fn_hs<T, false, false>(P.cw_u);
@@ -803,7 +804,9 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
         P.cw_u = (u == 4 || u == 16 || (u == 14 && P.cw_ring)) ? u : 8;
         P.cw_nt = env_int("CSRC_GPU_CW_NT", 128) == 256 ? 256 : 128;
         P.cw_pf = env_int("CSRC_GPU_CW_PF", 1);
-        if (P.cw_ring) P.cw_nt = dev::kCrRows;
+        P.cr_lr = P.cw_ring && env_int("CSRC_GPU_CR_LANES", 1) == 2 ? 2 : 1;
+        if (P.cw_ring) P.cw_nt = dev::kCrRows / P.cr_lr;
+        if (P.cr_lr == 2) P.cw_u = 8;  // the one two-lane shape: 8 pairs per lane, 16 per row and stage
         P.cr_stages = std::min(dev::kCrMaxStages, std::max(2, env_int("CSRC_GPU_CR_STAGES", 2)));
         P.cr_hint = env_int("CSRC_GPU_CR_HINT", 0) != 0;
         P.cr_split = env_int("CSRC_GPU_CR_SPLIT", 0) != 0;
@@ -814,9 +817,9 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     // ring form: bytes per stored pair, pairs per row a stage holds (one sub-chunk)
     const int64_t pair_bytes = 4 + static_cast<int64_t>(sizeof(T)) * (a.value_symmetric ? 1 : 2);
     const int ws_max = static_cast<int>(std::max<int64_t>(
-        1, static_cast<int64_t>(env_int("CSRC_GPU_CR_STAGE_BYTES", 33280)) / (dev::kCrRows * pair_bytes)));
+        1, static_cast<int64_t>(env_int("CSRC_GPU_CR_STAGE_BYTES", 33280 / P.cr_lr)) / (P.cw_nt * pair_bytes)));
     // (a copy chunk stages its kCrCopy row ids in the same ring)
-    P.cr_stage_bytes = std::max<int>(static_cast<int>(ws_max * dev::kCrRows * pair_bytes), dev::kCrCopy * 4);
+    P.cr_stage_bytes = std::max<int>(static_cast<int>(ws_max * P.cw_nt * pair_bytes), dev::kCrCopy * 4);
     // blocks of B rows, R = ceil(bw / B): rows more than R blocks apart never write the
     // same y position (row i writes only on [i - bw, i])
     const int r_target = std::min(15, std::max(1, env_int("CSRC_GPU_CW_R", P.cw_ring ? 2 : 4)));
@@ -1001,7 +1004,7 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     int d_default = 4 * R;
     if (ring) {
         const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", 400) / 100.0;
-        d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * dev::kCrRows) / static_cast<double>(B)));
+        d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * P.cw_nt) / static_cast<double>(B)));
     }
     const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", d_default));
     std::vector<int> order(P.cw_tasks);

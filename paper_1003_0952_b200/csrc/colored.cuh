@@ -334,9 +334,15 @@ constexpr int kCrConsumerRegs = 120;
 // so a consumer warp's chain per sub-chunk is one L2 round trip: wait full,
 // gather x / y, store, arrive done. The poll's round trip runs while the TMA is
 // in flight, the fence's while the consumers are on their next chunk.
-template <typename T, int U, bool HINT, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 3 : (U <= 4 ? 4 : (U <= 8 ? 3 : 2)))
+// LR lanes per row (1 or 2): a chunk holds RC = 128 / LR rows; with two lanes a row's pairs
+// are dealt round-robin (lane l takes pairs l, l + 2, ...), thread = row * 2 + lane, so the
+// half-batches of a warp's 16 rows are 128-byte segments and the lanes meet in one shuffle.
+template <typename T, int U, bool HINT, bool SPLIT, int LR = 1>
+__global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads,
+                                  SPLIT ? 3 : (LR == 2 ? 4 : (U <= 4 ? 4 : (U <= 8 ? 3 : 2))))
     k_colored_ring(ColorRingArgs<T> A) {
+    static_assert(LR == 1 || LR == 2, "one or two lanes per row");
+    constexpr int RC = kCrRows / LR;  // rows per class chunk
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kCrMaxStages];
     __shared__ __align__(8) uint64_t done[kCrMaxStages];
@@ -412,7 +418,7 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
                 hdr[s] = h;
                 mbar_arrive(&pub[s]);
                 if (nq) {
-                    const uint32_t bytes = static_cast<uint32_t>(nq) * kCrRows * eb;
+                    const uint32_t bytes = static_cast<uint32_t>(nq) * RC * eb;
                     mbar_expect_tx(&full[s], bytes);
                     tma_load_hint(smem_raw + static_cast<size_t>(s) * A.stage_bytes, src, bytes, &full[s], pol);
                     src += bytes;
@@ -502,10 +508,10 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
             if (h.task < 0) return;
             if (h.e >= 1 && h.e < A.n_e - 1 && h.nq > 0) {
                 const int32_t* sja = reinterpret_cast<const int32_t*>(smem_raw + static_cast<size_t>(s) * A.stage_bytes);
-                const int total = h.nq * kCrRows;
+                const int total = h.nq * RC;
                 for (int k = lane; k < total; k += 32) {
                     const int j = sja[k];
-                    if (j != h.r0 + (k & (kCrRows - 1))) {
+                    if (j != h.r0 + (k & (RC - 1))) {
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(A.xp + j));
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(A.yp + j));
                     }
@@ -562,42 +568,52 @@ __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads, SPLIT ? 
             for (int u = 0; u < kCrCopy / kCrRows; ++u)
                 if (i[u] >= 0) __stcs(A.y + i[u], v[u]);  // written once: streaming
         } else {
-            // one row per thread: colorful_worker's row update (parallel.hpp:411-434)
-            const bool act = r < h.r1;
+            // LR lanes per row: colorful_worker's row update (parallel.hpp:411-434)
+            const int rl = tid / LR, sub = tid % LR;
+            const int rc = h.r0 + rl;
+            const bool act = rc < h.r1;
             if (h.flags & 1) {
-                xi = act ? ld_w<HINT>(A.xp + r, pol) : T(0);
-                yown = act ? ld_w<HINT>(A.yp + r, pol) : T(0);  // no other row of this class writes y[r]
-                dr = act ? __ldcs(A.ad + r) : T(0);
+                xi = act ? ld_w<HINT>(A.xp + rc, pol) : T(0);
+                // (no other row of this class writes y[rc])
+                yown = act && sub == 0 ? ld_w<HINT>(A.yp + rc, pol) : T(0);
+                dr = act && sub == 0 ? __ldcs(A.ad + rc) : T(0);
                 acc = T(0);
             }
             const int nq = h.nq;
             const unsigned char* st = smem_raw + static_cast<size_t>(s) * A.stage_bytes;
-            const int32_t* sja = reinterpret_cast<const int32_t*>(st) + tid;
-            const T* sv0 = reinterpret_cast<const T*>(st + static_cast<size_t>(nq) * kCrRows * 4) + tid;
-            const T* sv1 = A.sym ? sv0 : sv0 + static_cast<size_t>(nq) * kCrRows;
+            const int32_t* sja = reinterpret_cast<const int32_t*>(st) + rl;
+            const T* sv0 = reinterpret_cast<const T*>(st + static_cast<size_t>(nq) * RC * 4) + rl;
+            const T* sv1 = A.sym ? sv0 : sv0 + static_cast<size_t>(nq) * RC;
             const T* sal = A.tr ? sv1 : sv0;
             const T* sau = A.tr ? sv0 : sv1;
-            for (int q0 = 0; q0 < nq; q0 += U) {
+            for (int k0 = 0; k0 * LR + sub < nq; k0 += U) {
                 int32_t j[U];
                 T xv[U], yv[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) j[u] = q0 + u < nq ? sja[(q0 + u) * kCrRows] : r;
+                for (int u = 0; u < U; ++u) {
+                    const int q = (k0 + u) * LR + sub;
+                    j[u] = q < nq ? sja[q * RC] : rc;
+                }
                 // padding entries (own row) neither gather nor scatter
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const bool real = j[u] != r;
+                    const bool real = j[u] != rc;
                     xv[u] = real ? ld_w<HINT>(A.xp + j[u], pol) : T(0);
                     yv[u] = real ? ld_w<HINT>(A.yp + j[u], pol) : T(0);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    if (j[u] != r) {
-                        acc = fma(sal[(q0 + u) * kCrRows], xv[u], acc);
-                        st_w<HINT>(A.yp + j[u], fma(sau[(q0 + u) * kCrRows], xi, yv[u]), pol);
+                    if (j[u] != rc) {
+                        const int q = (k0 + u) * LR + sub;
+                        acc = fma(sal[q * RC], xv[u], acc);
+                        st_w<HINT>(A.yp + j[u], fma(sau[q * RC], xi, yv[u]), pol);
                     }
                 }
             }
-            if ((h.flags & 2) && act) st_w<HINT>(A.yp + r, yown + fma(dr, xi, acc), pol);
+            if (h.flags & 2) {
+                if (LR == 2) acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+                if (act && sub == 0) st_w<HINT>(A.yp + rc, yown + fma(dr, xi, acc), pol);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&done[s]);  // stage free (loader), stores issued (signaller)

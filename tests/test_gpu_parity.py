@@ -868,6 +868,8 @@ COLORED_SHAPES = [
     {"CSRC_GPU_CR_SPLIT": "1", "CSRC_GPU_CW_U": "14"},                    # setmaxnreg register split
     {"CSRC_GPU_CR_PF": "1", "CSRC_GPU_CR_STAGES": "3"},                   # L2 prefetcher warp
     {"CSRC_GPU_CR_PF": "1", "CSRC_GPU_CR_STAGE_BYTES": "5120", "CSRC_GPU_CW_U": "4"},
+    {"CSRC_GPU_CR_LANES": "2"},                                           # two lanes per row, 64-row chunks
+    {"CSRC_GPU_CR_LANES": "2", "CSRC_GPU_CR_STAGE_BYTES": "3840", "CSRC_GPU_CR_STAGES": "4"},
     {"CSRC_GPU_CR_CLAIM": "1"},                                           # loader claims after staging
     {"CSRC_GPU_CR_CLAIM": "2", "CSRC_GPU_CR_STAGES": "3", "CSRC_GPU_CR_SLACK_PCT": "100"},
 ]
