@@ -67,7 +67,7 @@ typedef struct {
 enum {
     CSRC_KIND_SEQUENTIAL = 0,   /* no buffers: the gather kernel (windowed for band plans) */
     CSRC_KIND_LOCAL_BUFFERS = 1,/* windowed kernel into private band buffers + accumulation pass */
-    CSRC_KIND_COLORFUL = 2,     /* one launch per conflict-free row class, no atomics */
+    CSRC_KIND_COLORFUL = 2,     /* conflict-free row classes in class order, no atomics (one wavefront launch) */
     CSRC_KIND_ATOMIC = 3,       /* global fp64/fp32 red.global scatter baseline */
     CSRC_KIND_WINDOWED = 4,     /* TMA tiles, smem y rings, red.global flush (CSRC model bytes) */
     CSRC_KIND_GATHER = 5        /* transposed gather: the plan lays out each row's lower pairs and

@@ -208,19 +208,19 @@ __global__ void __launch_bounds__(NT, MINB) k_colored_wave(ColorWaveArgs<T> A) {
 
 // ---------------------------------------------------------------------------
 // Ring form of the wavefront (the default): the same (class, block) tasks,
-// tickets and dependency counters, but every CTA is warp-specialised. One
-// producer warp takes tickets ahead of time and streams each chunk's pairs --
-// packed per sub-chunk as [ja | al | au], SELL-128 -- into a shared-memory ring
-// with one TMA bulk copy per stage (L2 evict_first: the matrix is read once);
-// four consumer warps (one row per thread) wait for the stage, then for the
-// chunk's dependencies, and only then touch xp / yp in L2. The DRAM latency of
-// the matrix stream is therefore off the dependency path: the rows "in flight"
-// for the wavefront are just the ~300 chunks in their L2 read-add-write phase,
-// so class e can trail class e-1 by little more than the bandwidth and the
-// x / y window of all classes (~ (C + 2) (bw + in-flight rows) 16 B) stays
-// L2-resident. A control warp polls the dependencies ahead of the consumers and
-// publishes the completion counts behind them (need = 4 per chunk); there is no
-// CTA-wide barrier in the loop.
+// tickets and dependency counters, but every CTA is warp-specialised. A loader
+// warp takes tickets ahead of time and streams each chunk's pairs -- packed per
+// sub-chunk as [ja | al | au], SELL-128 -- into a shared-memory ring with one
+// TMA bulk copy per stage (L2 evict_first: the matrix is read once); a checker
+// warp polls the chunk's dependencies while the copy is in flight; four
+// consumer warps (one row per thread) wait for the stage and only then touch
+// xp / yp in L2; a signaller warp fences and publishes the completion count
+// behind them (need = 4 per chunk). The DRAM latency of the matrix stream is
+// therefore off the dependency path, and the traffic drops to 1.2x the model
+// (1.65x for the direct form); the x / y window of all classes is
+// ~ (C + 2) (bw + rows of the claimed, unfinished tickets) 16 B. There is no
+// CTA-wide barrier in the loop. Measured steps and the variants that lost:
+// DESIGN.md section 5.4, profiles/r02_colored_ring_sweeps.txt.
 constexpr int kCrRows = 128;       // rows per chunk = consumer threads
 constexpr int kCrWarps = kCrRows / 32;
 constexpr int kCrMaxStages = 6;
