@@ -627,5 +627,53 @@ CsrcRectResult decompose_rect(const M& a, int device = 0) {
     return r;
 }
 
+/// Multi-GPU band executor (csrc_gpu_band_exec_*, csrc_gpu.h): one per rank, one
+/// process per GPU. Rank `rank` of `world` owns a partition_by_nnz row band
+/// (partition.hpp:55-90); apply() runs the band product with its exchange over
+/// NCCL -- the windowed form's y-halo reduce into the owning ranks (the
+/// `effective` accumulation, parallel.hpp:371-382, at GPU granularity) or the
+/// gather form's x-halo refresh -- overlapped with the interior rows.
+///
+///     std::array<uint8_t, 128> id{};
+///     if (rank == 0) csrc::gpu::BandSpmv::unique_id(id.data());   // then broadcast id
+///     csrc::gpu::BandSpmv band(c, csrc::gpu::Strategy::windowed(), world, rank, id.data());
+///     band.apply(d_x, d_y, stream);       // x covers [x_lo, x_hi), y [y_lo, row_end)
+class BandSpmv {
+public:
+    enum class Form { windowed = CSRC_BAND_WINDOWED, gather = CSRC_BAND_GATHER };
+
+    /// ncclGetUniqueId on one rank (id: 128 bytes); the caller broadcasts it.
+    static void unique_id(uint8_t* id) { check(csrc_gpu_nccl_get_unique_id(id)); }
+
+    template <class M, class S>
+    BandSpmv(const M& a, const S& s, int world, int rank, const uint8_t* nccl_id, Form form = Form::windowed) {
+        const csrc_host_matrix m = view(a);
+        const csrc_gpu_strategy st = Strategy(s).c();
+        check(csrc_gpu_band_exec_create(&m, &st, world, rank, static_cast<int32_t>(form), nccl_id, &ex_));
+        check(csrc_gpu_band_exec_get_info(ex_, &lists_));
+    }
+    BandSpmv(const BandSpmv&) = delete;
+    BandSpmv& operator=(const BandSpmv&) = delete;
+    ~BandSpmv() {
+        if (ex_) csrc_gpu_band_exec_destroy(ex_);
+    }
+
+    /// Owned rows, the x / y ranges of the device vectors, messages per product.
+    const csrc_gpu_band_lists& lists() const { return lists_; }
+
+    /// y = A x on the band, exchange included, enqueued on `stream`
+    /// (refresh_x: the gather form's x-halo exchange before the boundary rows).
+    void apply(const void* d_x, void* d_y, void* stream = nullptr, bool refresh_x = false) {
+        check(csrc_gpu_band_exec_apply(ex_, d_x, d_y, stream, refresh_x ? 1 : 0));
+    }
+
+    /// ncclCommGetAsyncError: throws (communicator aborted) after a failure.
+    void check_comm() { check(csrc_gpu_band_exec_check(ex_)); }
+
+private:
+    csrc_gpu_band_exec_t ex_ = nullptr;
+    csrc_gpu_band_lists lists_{};
+};
+
 }  // namespace gpu
 }  // namespace csrc

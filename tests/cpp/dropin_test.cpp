@@ -171,6 +171,30 @@ int main() {
     } catch (const csrc::Error& e) {
         if (std::string(e.what()).find("sequential strategy requires p = 1") == std::string::npos) ++fails;
     }
+    // multi-GPU band executor wrapper (one rank: the band is the whole matrix). NCCL is
+    // loaded at run time by the library; without a loadable libnccl.so.2 this part is skipped.
+    {
+        CsrcMatrix c = csr_to_csrc(build_csr(generate_random_sym(200, 0.05, 11)));
+        uint8_t id[128] = {};
+        bool have_nccl = true;
+        try {
+            gpu::BandSpmv::unique_id(id);
+        } catch (const csrc::Error& e) {
+            have_nccl = false;
+            std::printf("dropin: band executor skipped (%s)\n", e.what());
+        }
+        if (have_nccl) {
+            for (auto form : {gpu::BandSpmv::Form::windowed, gpu::BandSpmv::Form::gather}) {
+                gpu::BandSpmv band(c, form == gpu::BandSpmv::Form::windowed ? gpu::Strategy::windowed()
+                                                                             : gpu::Strategy::gather(),
+                                   1, 0, id, form);
+                const csrc_gpu_band_lists& L = band.lists();
+                if (L.row_begin != 0 || L.row_end != static_cast<int32_t>(c.n) || L.n_sends != 0 || L.n_recvs != 0)
+                    ++fails;
+                band.check_comm();
+            }
+        }
+    }
     std::printf("dropin: max rel err %.3e, failures %d\n", worst, fails);
     return (worst <= 1e-12 && fails == 0) ? 0 : 1;
 }
