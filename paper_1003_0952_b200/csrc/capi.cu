@@ -596,7 +596,8 @@ void setup_windowed(Plan& P, const MatView& a, const std::vector<index_t>* expli
     const int max_st = std::min(env_int("CSRC_GPU_STAGES", 4), dev::kMaxStages);
     // 3 CTAs per SM (2 stages at C5) over 2 (3 stages): C5 sustained 0.896 vs 0.965 ms kernel
     // (100 products; the burst sweep of round 1 had preferred 2)
-    const int min_ctas = env_int("CSRC_GPU_MINCTAS", 3);
+    // fp32 stages are smaller: 4 CTAs per SM, C5 0.629 vs 0.658 ms (profiles/r02c_windowed_f32_shapes.txt)
+    const int min_ctas = env_int("CSRC_GPU_MINCTAS", sizeof(T) == 4 ? 4 : 3);
     for (int st = max_st; st >= 2; --st) {
         P.stages = st;
         size_rings(P, st);
