@@ -817,14 +817,30 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     const bool ring = P.cw_ring;
     // ring form: bytes per stored pair, pairs per row a stage holds (one sub-chunk)
     const int64_t pair_bytes = 4 + static_cast<int64_t>(sizeof(T)) * (a.value_symmetric ? 1 : 2);
-    const int ws_max = static_cast<int>(std::max<int64_t>(
-        1, static_cast<int64_t>(env_int("CSRC_GPU_CR_STAGE_BYTES", 33280 / P.cr_lr)) / (P.cw_nt * pair_bytes)));
+    // Stage size: what the longest row needs, up to 53,760 B (21 fp64 pairs per row). A
+    // 27-point row (13 pairs) takes one 33 KB fill; an elasticity row (40) two fills of 20
+    // instead of four of 10 (C4 0.99 vs 1.15 ms). Never larger than needed: shared memory
+    // comes out of the L1 that serves the row ids, diagonal and tickets (C5 with 54 KB
+    // stages: 1.31 vs 1.24 ms).
+    count_t w_max = 1;
+    for (index_t i = 0; i < n; ++i) w_max = std::max<count_t>(w_max, a.ia[i + 1] - a.ia[i]);
+    const int64_t row_slot = static_cast<int64_t>(P.cw_nt) * pair_bytes;  // bytes per pair slot of a chunk
+    const int64_t stage_cap = std::max<int64_t>(row_slot, env_int("CSRC_GPU_CR_STAGE_BYTES", 53760 / P.cr_lr));
+    const int64_t fills = (w_max * row_slot + stage_cap - 1) / stage_cap;
+    const int ws_max = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>((w_max + fills - 1) / fills, stage_cap / row_slot)));
     // (a copy chunk stages its kCrCopy row ids in the same ring)
     P.cr_stage_bytes = std::max<int>(static_cast<int>(ws_max * P.cw_nt * pair_bytes), dev::kCrCopy * 4);
     // blocks of B rows, R = ceil(bw / B): rows more than R blocks apart never write the
     // same y position (row i writes only on [i - bw, i])
     const int r_target = std::min(15, std::max(1, env_int("CSRC_GPU_CW_R", P.cw_ring ? 2 : 4)));
-    const int64_t min_rows = env_int("CSRC_GPU_CW_MINB", 32) * static_cast<int64_t>(C);
+    while (P.cr_stages > 2 && static_cast<int64_t>(P.cr_stages) * P.cr_stage_bytes > 200 * 1024) --P.cr_stages;
+    if (static_cast<int64_t>(P.cr_stages) * P.cr_stage_bytes > 220 * 1024)
+        throw Error("colorful: CSRC_GPU_CR_STAGE_BYTES exceeds the shared memory of an SM");
+    // rows per (block, class) task: at least four full chunks for the ring form (81 classes at
+    // C4: blocks of bw / 2 left 172 rows per task, one full and one third-full chunk; 0.88 vs
+    // 0.98 ms with four)
+    const int64_t min_rows = env_int("CSRC_GPU_CW_MINB", P.cw_ring ? 4 * dev::kCrRows : 32) * static_cast<int64_t>(C);
     int64_t B = std::max<int64_t>({(bw + r_target - 1) / r_target, min_rows, 256});
     B = std::min<int64_t>(B, std::max<index_t>(n, 1));
     const int NB = static_cast<int>((n + B - 1) / B);
@@ -1004,7 +1020,13 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
     const int grid_max = num_sms(P.device) * std::min(per_sm, std::max(occ, 1));
     int d_default = 4 * R;
     if (ring) {
-        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", 400) / 100.0;
+        // class distance = bandwidth + slack x the consumer rows: a CTA holds ~5 claimed,
+        // unfinished tickets, and 4x is the C5 optimum (more spills the window out of L2:
+        // profiles/r02_colored_ring_sweeps.txt); when x and y fit L2 whole there is nothing
+        // to spill and a wider distance only removes dependency waits (C3 0.50 vs 0.56 ms,
+        // C4 0.82 vs 0.88; profiles/r02c_colored_c2_c3_c4_defaults.txt)
+        const bool fits_l2 = 2.0 * static_cast<double>(npad) * sizeof(T) <= 96e6;
+        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", fits_l2 ? 800 : 400) / 100.0;
         d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * P.cw_nt) / static_cast<double>(B)));
     }
     const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", d_default));
