@@ -339,7 +339,7 @@ constexpr int kCrConsumerRegs = 120;
 // half-batches of a warp's 16 rows are 128-byte segments and the lanes meet in one shuffle.
 template <typename T, int U, bool HINT, bool SPLIT, int LR = 1>
 __global__ void __launch_bounds__(SPLIT ? kCrSplitThreads : kCrThreads,
-                                  SPLIT ? 3 : (LR == 2 ? 4 : (U <= 4 ? 4 : (U <= 8 ? 3 : 2))))
+                                  SPLIT ? 3 : (LR == 2 ? 4 : (U <= 4 ? 4 : ((U <= 8 || (sizeof(T) == 4 && U <= 14)) ? 3 : 2))))
     k_colored_ring(ColorRingArgs<T> A) {
     static_assert(LR == 1 || LR == 2, "one or two lanes per row");
     constexpr int RC = kCrRows / LR;  // rows per class chunk
