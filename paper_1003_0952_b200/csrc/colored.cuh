@@ -319,6 +319,8 @@ constexpr int kCrThreads = kCrRows + 128;  // consumers + loader, checker, signa
 // SM), the helper warpgroup drops to 40 and the consumers rise to 120, so the U = 14 / 16
 // forms (a whole 27-point row's gathers in flight: one L2 round trip per chunk) keep three
 // CTAs per SM instead of two.
+// (Measured slower, C5 1.58 vs 1.29 ms, and kept opt-in; a 56 / 112 split -- no spills in
+// the loader -- did not come up at all: the consumers' setmaxnreg.inc never got its registers.)
 constexpr int kCrSplitThreads = 2 * kCrRows;
 constexpr int kCrHelperRegs = 40;
 constexpr int kCrConsumerRegs = 120;
