@@ -22,6 +22,7 @@ def test_cpp_wrapper_header_compiles_standalone(tmp_path):
     """The wrapper needs only csrc_gpu.h when used with its own types."""
     src = tmp_path / "t.cpp"
     src.write_text('#include "csrc_gpu.hpp"\nint main(){ csrc::gpu::Strategy s = csrc::gpu::Strategy::windowed();'
+                   ' static_assert(sizeof(csrc::gpu::BandSpmv) > 0 && sizeof(csrc::gpu::ParallelSpmv) > 0, "");'
                    ' return s.kind == CSRC_KIND_WINDOWED ? 0 : 1; }\n')
     r = subprocess.run(["g++", "-std=c++17", "-I", os.path.join(ROOT, "include"), str(src), "-o",
                         str(tmp_path / "t")], capture_output=True, text=True)
