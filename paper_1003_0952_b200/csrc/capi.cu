@@ -1023,10 +1023,10 @@ void setup_colored_wave(Plan& P, const MatView& a, const std::vector<int32_t>& c
         // class distance = bandwidth + slack x the consumer rows: a CTA holds ~5 claimed,
         // unfinished tickets, and 4x is the C5 optimum (more spills the window out of L2:
         // profiles/r02_colored_ring_sweeps.txt); when x and y fit L2 whole there is nothing
-        // to spill and a wider distance only removes dependency waits (C3 0.50 vs 0.56 ms,
-        // C4 0.82 vs 0.88; profiles/r02c_colored_c2_c3_c4_defaults.txt)
+        // to spill and a wider distance only removes dependency waits (16x: C3 0.47 vs 0.56 ms,
+        // C4 0.76 vs 0.88; profiles/r02c_colored_c2_c3_c4_defaults.txt); fp32 halves the window bytes
         const bool fits_l2 = 2.0 * static_cast<double>(npad) * sizeof(T) <= 96e6;
-        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", fits_l2 ? 800 : 400) / 100.0;
+        const double slack = env_int("CSRC_GPU_CR_SLACK_PCT", fits_l2 ? 1600 : (sizeof(T) == 4 ? 600 : 400)) / 100.0;
         d_default = static_cast<int>(std::ceil((static_cast<double>(bw) + slack * grid_max * P.cw_nt) / static_cast<double>(B)));
     }
     const int D = std::max(R + 1, env_int("CSRC_GPU_CW_D", d_default));
