@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(NT, MINB) k_colored_wave(ColorWaveArgs<T> A) {
 // consumer warps (one row per thread) wait for the stage and only then touch
 // xp / yp in L2; a signaller warp fences and publishes the completion count
 // behind them (need = 4 per chunk). The DRAM latency of the matrix stream is
-// therefore off the dependency path, and the traffic drops to 1.2x the model
+// therefore off the dependency path, and the traffic drops to 1.2-1.3x the model
 // (1.65x for the direct form); the x / y window of all classes is
 // ~ (C + 2) (bw + rows of the claimed, unfinished tickets) 16 B. There is no
 // CTA-wide barrier in the loop. Measured steps and the variants that lost:
